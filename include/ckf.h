@@ -1,0 +1,143 @@
+/*
+ * ckf.h -- C ABI of the B200-native cuckoo-filter hot path (libckf.so).
+ *
+ * This is the drop-in boundary.  The reference (swarcuckoo 0.1.0) crosses
+ * from Python into compiled code at the numba batch kernels; each entry point
+ * below replaces one of them (file:line in /root/reference/pkg/src/swarcuckoo):
+ *
+ *   ckf_params_init   <- FilterConfig.__post_init__ + CuckooFilter._kargs
+ *                        (placement.py:77-136, filter.py:133-154)
+ *   ckf_hash          <- _kernels.hash_batch    (_kernels.py:489-493)
+ *   ckf_place         <- _kernels.place_batch   (_kernels.py:496-507)
+ *   ckf_insert        <- _kernels.insert_batch  (_kernels.py:510-529)
+ *   ckf_query         <- _kernels.query_batch   (_kernels.py:532-537)
+ *   ckf_delete        <- _kernels.delete_batch  (_kernels.py:540-549)
+ *   ckf_host_place    <- placement.derive_placement (placement.py:219-232),
+ *                        host-compiled from the same header the kernels use
+ *
+ * Conventions:
+ *  - every pointer argument except `p` and the host_* helpers is DEVICE memory
+ *    owned by the caller (torch tensors in the Python facade); nothing here
+ *    allocates;
+ *  - every call is asynchronous on `stream` (a cudaStream_t passed as void*;
+ *    NULL = legacy default stream);
+ *  - return 0 on success, CKF_EINVAL for bad arguments, or
+ *    CKF_ECUDA_BASE - cudaError_t for a CUDA launch error; ckf_strerror()
+ *    names the code.  Kernels never fail per key: "full" and "not found"
+ *    are data, exactly as in the reference (_kernels.py:388-389).
+ */
+#ifndef CKF_H_
+#define CKF_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define CKF_ABI_VERSION 1
+
+#define CKF_OK 0
+#define CKF_EINVAL (-22)
+#define CKF_ECUDA_BASE (-1000)
+
+#define CKF_POLICY_XOR 0
+#define CKF_POLICY_OFFSET 1
+#define CKF_EVICT_DFS 0
+#define CKF_EVICT_BFS 1
+
+/* op flags */
+#define CKF_MODE_CONCURRENT 0u   /* lock-free, one thread per key (default) */
+#define CKF_MODE_SEQUENTIAL 1u   /* one device thread, reference key order:
+                                    bit-identical to insert_batch(workers=1) */
+#define CKF_INPUT_HASHED 2u      /* `keys` already holds xxh64(key, seed) */
+
+/* Filter geometry: the reference `_kargs` tuple (filter.py:150-154) plus the
+ * eviction knobs; filled and validated by ckf_params_init. Passed by pointer,
+ * read on the host, copied into the kernel launch by value. */
+typedef struct ckf_params {
+  uint64_t seed;
+  uint64_t bucket_count;      /* m */
+  uint64_t index_mask;        /* m-1 for power-of-two m, else 0 */
+  uint64_t high;              /* per-lane MSB mask */
+  uint64_t choice_bit;        /* 1<<(f-1) for offset, 0 for xor */
+  uint64_t delta_magic;       /* fastmod constant for tag_hash % (m-1) (offset) */
+  uint64_t worker;            /* eviction PRNG stream id (filter.py:285) */
+  uint32_t fingerprint_bits;  /* f in {8,16,32} */
+  uint32_t bucket_slots;      /* b */
+  uint32_t words_per_bucket;  /* b*f/64 */
+  uint32_t tags_per_word;     /* 64/f */
+  uint32_t payload_bits;      /* f (xor) or f-1 (offset) */
+  uint32_t policy;            /* CKF_POLICY_* */
+  uint32_t eviction;          /* CKF_EVICT_* */
+  uint32_t max_evictions;     /* >= 1 */
+} ckf_params;
+
+/* Sparse per-key insert outcome for keys that needed the eviction path
+ * (evictions >= 1 or failure).  Keys placed directly have evictions == 0 and
+ * lost == 0 and produce no record; this is how the facade rebuilds the
+ * reference BatchInsertResult (filter.py:95-112) without 16 B/key of dense
+ * output traffic. */
+typedef struct ckf_record {
+  uint64_t index;      /* position of the key in the batch */
+  uint64_t lost;       /* payload fingerprint dropped on failure, else 0 */
+  uint32_t evictions;  /* eviction rounds (max_evictions on failure) */
+  uint32_t ok;         /* 1 stored, 0 failed */
+} ckf_record;
+
+/* Device-side counters of one call; zeroed by the call itself. */
+typedef struct ckf_counters {
+  unsigned long long n_ok;         /* successful inserts / deletes */
+  unsigned long long n_records;    /* records produced (may exceed capacity) */
+  unsigned long long n_queued;     /* keys that entered the eviction pass */
+  unsigned long long reserved;
+} ckf_counters;
+
+int ckf_abi_version(void);
+const char* ckf_strerror(int code);
+
+/* Validates like FilterConfig (placement.py:77-102) and derives geometry. */
+int ckf_params_init(ckf_params* p, uint64_t bucket_count, uint32_t fingerprint_bits,
+                    uint32_t bucket_slots, int policy, int eviction, uint32_t max_evictions,
+                    uint64_t seed);
+
+/* out[i] = xxh64(keys[i], seed) */
+int ckf_hash(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, void* stream);
+
+/* (fp, i1, i2) per key; flags may carry CKF_INPUT_HASHED. */
+int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* fp, uint64_t* i1,
+              uint64_t* i2, unsigned flags, void* stream);
+
+/* Batch insert.  ok[n] is required.  evictions/lost are optional DENSE
+ * outputs with the reference's types (int64 / uint64 per key).  records
+ * (capacity record_cap) receives the sparse outcomes and doubles as the
+ * eviction work queue; if it overflows, the excess keys are evicted in place
+ * and only counted.  occupancy (nullable) is atomically increased by n_ok. */
+int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n,
+               uint8_t* ok, int64_t* evictions, uint64_t* lost, ckf_record* records,
+               uint64_t record_cap, ckf_counters* counters, long long* occupancy,
+               unsigned flags, void* stream);
+
+/* Batch membership; out[i] in {0,1}.  Read-only phase (filter.py:9-15). */
+int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, uint64_t n,
+              uint8_t* out, unsigned flags, void* stream);
+
+/* Batch delete; out[i] = 1 where a lane was cleared.  occupancy (nullable)
+ * is atomically decreased by n_ok. */
+int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n,
+               uint8_t* out, ckf_counters* counters, long long* occupancy, unsigned flags,
+               void* stream);
+
+/* Host-compiled copies of the shared device semantics (same source as the
+ * kernels); used by derive_placement() and by the CPU parity tests. */
+uint64_t ckf_host_hash(uint64_t key, uint64_t seed);
+void ckf_host_place(const ckf_params* p, uint64_t key, uint64_t* fp, uint64_t* i1, uint64_t* i2);
+uint64_t ckf_host_alt(const ckf_params* p, uint64_t bucket, uint64_t fp, uint64_t choice,
+                      uint64_t* new_choice);
+uint64_t ckf_host_zero_mask(uint32_t fingerprint_bits, uint64_t word);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* CKF_H_ */

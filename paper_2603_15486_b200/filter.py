@@ -1,0 +1,459 @@
+"""``CuckooFilter`` -- the drop-in facade over the sm_100a kernels.
+
+Same public API as the reference ``swarcuckoo.filter.CuckooFilter``
+(/root/reference/pkg/src/swarcuckoo/filter.py:115-574): batch
+``insert_batch / query_batch / delete_batch``, scalar ``insert / query /
+delete``, ``occupancy / load_factor / len / in``, ``clear``, ``stored_tags``,
+``collect_eviction_stats`` and CKGF ``to_bytes / from_bytes / save / load``.
+
+What differs is where the state lives and who runs the loops:
+
+* the word table is a torch ``int64`` tensor of ``m * wpb`` words in HBM
+  (reinterpreted as uint64 by the kernels), 256-byte aligned so every
+  f=16/b=16 bucket is one 32-byte sector;
+* every batch call is ONE C-ABI call (``libckf.so``) enqueued on the current
+  CUDA stream -- no per-key Python, no CPU fallback;
+* occupancy is a device counter updated by the kernels (the paper's
+  hierarchical count) instead of per-worker dict shards;
+* keys may be numpy arrays / sequences (results come back as numpy, exactly
+  like the reference) or torch tensors (results stay torch, on the device).
+
+``workers`` is accepted for compatibility and ignored: the GPU runs one
+thread per key.  ``deterministic=True`` selects the single-device-thread
+parity mode, bit-identical to the reference ``workers=1`` batch loop
+(filter.py:416-421).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import struct
+from dataclasses import dataclass
+from typing import NamedTuple, Optional
+
+import numpy as np
+import torch
+
+from . import _lib
+from .config import Eviction, FilterConfig, MASK64, Policy
+from .errors import PhaseError
+
+_MAGIC = b"CKGF"
+_VERSION = 1
+# magic, version, f, b, m, policy, occupancy, seed (filter.py:38-42)
+_HEADER = struct.Struct("<4sIIIQIQQ")
+
+_REC_DTYPE = np.dtype([("index", "<u8"), ("lost", "<u8"), ("evictions", "<u4"), ("ok", "<u4")])
+assert _REC_DTYPE.itemsize == _lib.RECORD_BYTES
+
+
+class InsertResult(NamedTuple):
+    """Outcome of one insert (filter.py:45-58)."""
+
+    ok: bool
+    evictions: int
+    lost_fingerprint: Optional[int] = None
+
+    def __bool__(self) -> bool:
+        return self.ok
+
+
+@dataclass
+class EvictionStats:
+    """Per-insert eviction-round counts with percentile readout (filter.py:61-92)."""
+
+    samples: np.ndarray
+    failures: int = 0
+
+    def percentile(self, p: float) -> int:
+        if len(self.samples) == 0:
+            return 0
+        return int(np.percentile(self.samples, p, method="inverted_cdf"))
+
+    @property
+    def p90(self) -> int:
+        return self.percentile(90)
+
+    @property
+    def p95(self) -> int:
+        return self.percentile(95)
+
+    @property
+    def p99(self) -> int:
+        return self.percentile(99)
+
+    @property
+    def mean(self) -> float:
+        return float(self.samples.mean()) if len(self.samples) else 0.0
+
+    @property
+    def max(self) -> int:
+        return int(self.samples.max()) if len(self.samples) else 0
+
+
+class BatchInsertResult:
+    """Index-aligned per-key insert outcomes (filter.py:95-112).
+
+    The kernels write a dense ``ok`` byte per key plus sparse records for
+    the keys that went through the eviction pass; ``evictions`` and
+    ``lost_fingerprints`` are rebuilt from those records on first access
+    (directly placed keys have 0 evictions and nothing lost).  Arrays are numpy
+    when the keys were host data and torch device tensors when they were a
+    CUDA tensor.
+    """
+
+    def __init__(self, n: int, ok_dev: torch.Tensor, records: torch.Tensor, counters: torch.Tensor,
+                 as_numpy: bool):
+        self._n = n
+        self._ok_dev = ok_dev
+        self._rec = records
+        self._ctr = counters
+        self._numpy = as_numpy
+        self._ok = None
+        self._ev = None
+        self._lost = None
+        self._nrec = None
+
+    # -- device-side summaries (one tiny D2H each) --
+    def _counts(self):
+        if self._nrec is None:
+            c = self._ctr.cpu()
+            self._nok_cached = int(c[0])
+            self._nrec = int(c[1])
+        return self._nok_cached, self._nrec
+
+    @property
+    def n_ok(self) -> int:
+        return self._counts()[0]
+
+    @property
+    def n_failed(self) -> int:
+        return self._n - self.n_ok
+
+    def records(self) -> np.ndarray:
+        """The sparse (index, lost, evictions, ok) records, host structured array."""
+        nrec = self._counts()[1]
+        raw = self._rec[: nrec * _lib.RECORD_BYTES].cpu().numpy()
+        return raw.view(_REC_DTYPE)
+
+    @property
+    def ok(self):
+        if self._ok is None:
+            okb = self._ok_dev.view(torch.bool)
+            self._ok = okb.cpu().numpy() if self._numpy else okb
+        return self._ok
+
+    def _expand(self):
+        rec = self.records()
+        ev = np.zeros(self._n, dtype=np.int64)
+        lost = np.zeros(self._n, dtype=np.uint64)
+        if len(rec):
+            idx = rec["index"].astype(np.int64)
+            ev[idx] = rec["evictions"]
+            lost[idx] = rec["lost"]
+        if self._numpy:
+            self._ev, self._lost = ev, lost
+        else:
+            dev = self._ok_dev.device
+            self._ev = torch.from_numpy(ev).to(dev)
+            self._lost = torch.from_numpy(lost.view(np.int64)).to(dev)
+
+    @property
+    def evictions(self):
+        if self._ev is None:
+            self._expand()
+        return self._ev
+
+    @property
+    def lost_fingerprints(self):
+        if self._lost is None:
+            self._expand()
+        return self._lost
+
+    def eviction_stats(self) -> EvictionStats:
+        ev = self.evictions
+        ev = ev.cpu().numpy() if isinstance(ev, torch.Tensor) else ev.copy()
+        return EvictionStats(ev, failures=self.n_failed)
+
+
+def _default_device() -> torch.device:
+    if not torch.cuda.is_available():
+        raise RuntimeError("CuckooFilter needs a CUDA device (B200); no CPU fallback exists")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+class CuckooFilter:
+    """GPU cuckoo filter with packed SWAR buckets and lock-free CAS updates.
+
+    >>> filt = CuckooFilter(FilterConfig(bucket_count=1 << 10))
+    >>> filt.insert(42).ok, 42 in filt, filt.delete(42)
+    (True, True, True)
+    """
+
+    def __init__(self, cfg: FilterConfig, *, debug_phase: bool = False, device=None,
+                 deterministic: bool = False):
+        self.cfg = cfg
+        self.device = torch.device(device) if device is not None else _default_device()
+        if self.device.type != "cuda":
+            raise RuntimeError("CuckooFilter runs on CUDA devices only")
+        self._params = cfg.ckf_params()
+        self._deterministic = deterministic
+        with torch.cuda.device(self.device):
+            self.words_device = torch.zeros(cfg.total_words, dtype=torch.int64, device=self.device)
+            # [0] occupancy (kernels add/subtract), [1..4] scratch counters for scalar ops
+            self._occ = torch.zeros(1, dtype=torch.int64, device=self.device)
+            self._ctr = torch.zeros(4, dtype=torch.int64, device=self.device)
+        self._debug = debug_phase
+        self._mut_depth = 0
+        self._read_depth = 0
+
+    # ---- bookkeeping ----
+
+    @property
+    def occupancy(self) -> int:
+        """Stored-item count: successful inserts minus successful deletes."""
+        return int(self._occ.item())
+
+    @property
+    def load_factor(self) -> float:
+        return self.occupancy / self.cfg.total_slots
+
+    def __len__(self) -> int:
+        return self.occupancy
+
+    def __contains__(self, key: int) -> bool:
+        return self.query(key)
+
+    def __repr__(self) -> str:
+        c = self.cfg
+        return (f"CuckooFilter(f={c.fingerprint_bits}, b={c.bucket_slots}, m={c.bucket_count}, "
+                f"policy={c.policy.value}, eviction={c.eviction.value}, occupancy={self.occupancy}, "
+                f"device={self.device})")
+
+    @property
+    def words(self) -> np.ndarray:
+        """Host snapshot of the word table as uint64 (the reference attribute)."""
+        return self.words_device.cpu().numpy().view(np.uint64)
+
+    def clear(self) -> None:
+        self.words_device.zero_()
+        self._occ.zero_()
+
+    def stored_tags(self) -> np.ndarray:
+        """(m, b) uint64 snapshot of every lane, 0 = empty (filter.py:194-208)."""
+        c = self.cfg
+        f, tpw = c.fingerprint_bits, c.tags_per_word
+        w = self.words_device.view(c.bucket_count, c.words_per_bucket)
+        lanes = torch.empty((c.bucket_count, c.bucket_slots), dtype=torch.int64, device=self.device)
+        mask = (1 << f) - 1
+        for slot in range(c.bucket_slots):
+            lanes[:, slot] = torch.bitwise_and(w[:, slot // tpw] >> (f * (slot % tpw)), mask)
+        return lanes.cpu().numpy().view(np.uint64)
+
+    # ---- phase assertions (debug mode only; filter.py:212-226) ----
+
+    def _enter_mutate(self) -> None:
+        if self._read_depth:
+            raise PhaseError("mutation started while queries are in flight")
+        self._mut_depth += 1
+
+    def _exit_mutate(self) -> None:
+        self._mut_depth -= 1
+
+    def _enter_read(self) -> None:
+        if self._mut_depth:
+            raise PhaseError("query started while mutations are in flight")
+        self._read_depth += 1
+
+    def _exit_read(self) -> None:
+        self._read_depth -= 1
+
+    # ---- plumbing ----
+
+    def _stream(self) -> int:
+        return torch.cuda.current_stream(self.device).cuda_stream
+
+    def _as_keys(self, keys):
+        """Contiguous device int64 view of the keys + whether to answer in numpy."""
+        if isinstance(keys, torch.Tensor):
+            if keys.dim() != 1:
+                raise ValueError("keys must be one-dimensional")
+            if keys.dtype == torch.uint64:
+                keys = keys.view(torch.int64)
+            elif keys.dtype != torch.int64:
+                keys = keys.to(torch.int64)
+            if keys.device != self.device:
+                return keys.to(self.device, non_blocking=True).contiguous(), False
+            return keys.contiguous(), False
+        arr = np.ascontiguousarray(keys, dtype=np.uint64)
+        if arr.ndim != 1:
+            raise ValueError("keys must be one-dimensional")
+        t = torch.from_numpy(arr.view(np.int64))
+        return t.to(self.device), True
+
+    def _flags(self, deterministic: Optional[bool]) -> int:
+        det = self._deterministic if deterministic is None else deterministic
+        return _lib.MODE_SEQUENTIAL if det else _lib.MODE_CONCURRENT
+
+    def _params_for(self, worker: int):
+        if worker == 0:
+            return self._params
+        p = _lib.Params.from_buffer_copy(self._params)
+        p.worker = worker & MASK64
+        return p
+
+    # ---- scalar operations ----
+
+    def insert(self, key: int, worker: int = 0) -> InsertResult:
+        """Store one key; evict residents if both buckets are full (filter.py:230-240)."""
+        if self._debug:
+            self._enter_mutate()
+        try:
+            res = self._insert(np.array([key & MASK64], dtype=np.uint64), worker, None)
+            ev = int(res.evictions[0])
+            if bool(res.ok[0]):
+                return InsertResult(True, ev)
+            return InsertResult(False, ev, int(res.lost_fingerprints[0]))
+        finally:
+            if self._debug:
+                self._exit_mutate()
+
+    def query(self, key: int) -> bool:
+        if self._debug:
+            self._enter_read()
+        try:
+            return bool(self._query(np.array([key & MASK64], dtype=np.uint64))[0])
+        finally:
+            if self._debug:
+                self._exit_read()
+
+    def delete(self, key: int, worker: int = 0) -> bool:
+        """Clear one lane matching the key's fingerprint (filter.py:252-264)."""
+        if self._debug:
+            self._enter_mutate()
+        try:
+            return bool(self._delete(np.array([key & MASK64], dtype=np.uint64), None)[0])
+        finally:
+            if self._debug:
+                self._exit_mutate()
+
+    # ---- batch operations ----
+
+    def insert_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None) -> BatchInsertResult:
+        """Insert every key; results are index-aligned with the input (filter.py:401-442)."""
+        if self._debug:
+            self._enter_mutate()
+        try:
+            return self._insert(keys, 0, deterministic)
+        finally:
+            if self._debug:
+                self._exit_mutate()
+
+    def query_batch(self, keys, workers: int = 1):
+        """Boolean membership per key (filter.py:444-473)."""
+        if self._debug:
+            self._enter_read()
+        try:
+            return self._query(keys)
+        finally:
+            if self._debug:
+                self._exit_read()
+
+    def delete_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None):
+        """Delete each key once; True where a matching lane was cleared (filter.py:475-502)."""
+        if self._debug:
+            self._enter_mutate()
+        try:
+            return self._delete(keys, deterministic)
+        finally:
+            if self._debug:
+                self._exit_mutate()
+
+    def _insert(self, keys, worker: int, deterministic: Optional[bool]) -> BatchInsertResult:
+        k, as_np = self._as_keys(keys)
+        n = k.numel()
+        with torch.cuda.device(self.device):
+            ok = torch.empty(n, dtype=torch.uint8, device=self.device)
+            rec = torch.empty(max(n, 1) * _lib.RECORD_BYTES, dtype=torch.uint8, device=self.device)
+            ctr = torch.empty(4, dtype=torch.int64, device=self.device)
+            p = self._params_for(worker)
+            _lib.check(_lib.lib().ckf_insert(
+                ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, ok.data_ptr(),
+                None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(),
+                self._flags(deterministic), self._stream()))
+        return BatchInsertResult(n, ok, rec, ctr, as_np)
+
+    def _query(self, keys):
+        k, as_np = self._as_keys(keys)
+        n = k.numel()
+        with torch.cuda.device(self.device):
+            out = torch.empty(n, dtype=torch.uint8, device=self.device)
+            _lib.check(_lib.lib().ckf_query(
+                ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
+                out.data_ptr(), 0, self._stream()))
+        res = out.view(torch.bool)
+        return res.cpu().numpy() if as_np else res
+
+    def _delete(self, keys, deterministic: Optional[bool]):
+        k, as_np = self._as_keys(keys)
+        n = k.numel()
+        with torch.cuda.device(self.device):
+            out = torch.empty(n, dtype=torch.uint8, device=self.device)
+            _lib.check(_lib.lib().ckf_delete(
+                ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
+                out.data_ptr(), self._ctr.data_ptr(), self._occ.data_ptr(),
+                self._flags(deterministic), self._stream()))
+        res = out.view(torch.bool)
+        return res.cpu().numpy() if as_np else res
+
+    def collect_eviction_stats(self, keys, prefill_fraction: float = 0.75, workers: int = 1) -> EvictionStats:
+        """Insert all keys, sampling eviction counts past the prefill (filter.py:504-519)."""
+        if not 0.0 <= prefill_fraction < 1.0:
+            raise ValueError("prefill_fraction must be in [0, 1)")
+        k, _ = self._as_keys(keys)
+        cut = int(k.numel() * prefill_fraction)
+        if cut:
+            self.insert_batch(k[:cut], workers=workers)
+        tail = self.insert_batch(k[cut:], workers=workers)
+        return tail.eviction_stats()
+
+    # ---- CKGF serialization (filter.py:523-574) ----
+
+    def to_bytes(self) -> bytes:
+        c = self.cfg
+        header = _HEADER.pack(_MAGIC, _VERSION, c.fingerprint_bits, c.bucket_slots, c.bucket_count,
+                              0 if c.policy is Policy.XOR else 1, self.occupancy, c.seed)
+        return header + self.words.astype("<u8", copy=False).tobytes()
+
+    def save(self, path) -> None:
+        with open(path, "wb") as fh:
+            fh.write(self.to_bytes())
+
+    @classmethod
+    def from_bytes(cls, data: bytes, *, eviction=Eviction.DFS, max_evictions: int = 500,
+                   device=None) -> "CuckooFilter":
+        if len(data) < _HEADER.size:
+            raise ValueError("truncated filter dump: header incomplete")
+        magic, version, f, b, m, pol, occupancy, seed = _HEADER.unpack_from(data)
+        if magic != _MAGIC:
+            raise ValueError(f"bad magic {magic!r}, expected {_MAGIC!r}")
+        if version != _VERSION:
+            raise ValueError(f"unsupported dump version {version}")
+        if pol not in (0, 1):
+            raise ValueError(f"unknown policy code {pol}")
+        cfg = FilterConfig(bucket_count=m, fingerprint_bits=f, bucket_slots=b,
+                           policy=Policy.XOR if pol == 0 else Policy.OFFSET,
+                           eviction=eviction, max_evictions=max_evictions, seed=seed)
+        body = memoryview(data)[_HEADER.size:]
+        if len(body) != cfg.total_words * 8:
+            raise ValueError(f"word array is {len(body)} bytes, expected {cfg.total_words * 8}")
+        filt = cls(cfg, device=device)
+        host = torch.from_numpy(np.frombuffer(body, dtype="<u8").view(np.int64).copy())
+        filt.words_device.copy_(host)
+        filt._occ.fill_(occupancy)
+        return filt
+
+    @classmethod
+    def load(cls, path, **kwargs) -> "CuckooFilter":
+        with open(path, "rb") as fh:
+            return cls.from_bytes(fh.read(), **kwargs)
