@@ -1,0 +1,401 @@
+#!/usr/bin/env python
+"""Benchmark of the cuckoo-filter hot path (BASELINE.json configs[1]).
+
+One STEP = the reference's throughput protocol (swarcuckoo/bench.py:149-197)
+over one batch on a 2^28-slot f=16 b=16 table:
+    insert n = floor(0.95 * 2^28) keys into the empty table (0 -> 95% load)
+    lookup+  the same n keys
+    lookup-  n disjoint negative keys
+    delete   the n keys (table back to empty, so steps chain without a clear)
+Keys are the reference's gen_keys streams (Philox; positives in [0,2^32),
+negatives in [2^32,2^64)), generated once and resident in HBM before timing.
+`value` = 4n ops / device time per step, in billion ops/s, max over ranks.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Multi-GPU (torchrun, one rank per GPU): weak scaling, 2^28 slots per GPU;
+each rank owns one hash shard and generates n keys, which are routed to their
+owning GPU with NCCL all-to-all (paper_2603_15486_b200/sharded.py).
+
+`--impl reference` times the reference algorithm on the host CPU cores (the
+C restatement in oracle/, the reference itself being a numba package that
+does not ship to the GPU box), on a bounded 2^24-slot sample per step.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+from pathlib import Path
+
+import numpy as np
+
+ROOT = Path(__file__).resolve().parent
+sys.path.insert(0, str(ROOT))
+
+METRIC = "insert/lookup/delete billion ops/s at 95% load; fraction of HBM roofline"
+UNIT = "B ops/s"
+KEY_SPLIT = 1 << 32
+
+
+def gen_keys(n: int, seed: int, negative: bool = False) -> np.ndarray:
+    """The reference's key streams (swarcuckoo/bench.py:101-106)."""
+    rng = np.random.Generator(np.random.Philox(key=[seed, int(negative)]))
+    if negative:
+        return rng.integers(KEY_SPLIT, 1 << 64, size=n, dtype=np.uint64)
+    return rng.integers(0, KEY_SPLIT, size=n, dtype=np.uint64)
+
+
+def measured_peaks() -> dict:
+    p = ROOT / "MEASURED_PEAKS.json"
+    if p.exists():
+        d = json.loads(p.read_text())
+        return {"hbm_gbs": float(d["hbm_gbs"]), "source": "measured (MEASURED_PEAKS.json)"}
+    return {"hbm_gbs": 6650.0, "source": "fallback (B200_PROFILING.md)"}
+
+
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.index}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "100"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+        return self
+
+    def __exit__(self, *exc):
+        self.lines = []
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                out, _ = self.proc.communicate(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+                out, _ = self.proc.communicate()
+            self.lines = [ln for ln in out.splitlines() if ln.strip()]
+
+    def summary(self) -> dict:
+        sm, smax, reasons = [], 0.0, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in getattr(self, "lines", []):
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                smax = max(smax, float(f[2]))
+            except ValueError:
+                continue
+            for name, val in zip(names, f[5:9]):
+                if val.lower() == "active":
+                    reasons.add(name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": smax or None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# --------------------------------------------------------------------------
+# CPU reference arm (oracle/ = C restatement of swarcuckoo's kernels)
+# --------------------------------------------------------------------------
+
+def cpu_protocol(log2_slots: int, pos: np.ndarray, neg: np.ndarray, threads: int) -> dict:
+    """One pass of the step protocol on the CPU: insert (1 thread, like the
+    reference's fused workers=1 kernel), lookup+/- (`threads` threads, like its
+    nogil query workers), delete (1 thread)."""
+    import oracle
+
+    cfg = oracle.make_cfg(1 << (log2_slots - 4), 16, 16, "xor", "bfs", 500, 0)
+    n = int(0.95 * (1 << log2_slots))
+    p, q = pos[:n], neg[:n]
+    filt = oracle.OracleFilter(cfg)
+    t0 = time.perf_counter()
+    ok, _, _ = filt.insert_batch(p)
+    t1 = time.perf_counter()
+    hp = filt.query_batch(p, threads=threads)
+    t2 = time.perf_counter()
+    hn = filt.query_batch(q, threads=threads)
+    t3 = time.perf_counter()
+    filt.delete_batch(p)
+    t4 = time.perf_counter()
+    assert ok.all() and hp.all() and filt.occupancy == 0
+    total = t4 - t0
+    return {"n": n, "seconds": total, "value": 4 * n / total / 1e9,
+            "per_op_Mops": {"insert": n / (t1 - t0) / 1e6, "lookup+": n / (t2 - t1) / 1e6,
+                            "lookup-": n / (t3 - t2) / 1e6, "delete": n / (t4 - t3) / 1e6},
+            "fpr": float(hn.mean())}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def run_reference(args) -> None:
+    rank = int(os.environ.get("RANK", 0))
+    if rank != 0:
+        return
+    import oracle
+
+    oracle.build()
+    threads = host_threads()
+    n = int(0.95 * (1 << args.cpu_log2_slots))
+    pos, neg = gen_keys(n, 0), gen_keys(n, 0, negative=True)
+    for _ in range(args.warmup):
+        cpu_protocol(args.cpu_log2_slots, pos, neg, threads)
+    runs = [cpu_protocol(args.cpu_log2_slots, pos, neg, threads) for _ in range(args.steps)]
+    secs = [r["seconds"] for r in runs]
+    value = 4 * n * len(runs) / sum(secs) / 1e9
+    sample = (f"per step: the step protocol on a 2^{args.cpu_log2_slots}-slot f=16 b=16 xor/bfs table "
+              f"(n={n} keys, same gen_keys streams); insert/delete 1 thread, lookups {threads} threads")
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
+        "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
+        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+        "data": "synthetic (reference gen_keys Philox streams)",
+        "config": {"workload": f"cuckoo filter step protocol, 2^{args.cpu_log2_slots} slots sample of configs[1]",
+                   "fingerprint_bits": 16, "bucket_slots": 16, "policy": "xor", "eviction": "bfs",
+                   "load_factor": 0.95, "keys_per_step": 4 * n},
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+        "per_op_Mops": runs[-1]["per_op_Mops"],
+    }
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------
+# GPU arm
+# --------------------------------------------------------------------------
+
+def alg_bytes(op: str, S: int, p2: float) -> float:
+    """Algorithmic bytes per op (BASELINE.md §2 / SURVEY.md §8(d))."""
+    if op == "lookup-":
+        return 8 + 1 + 2 * S
+    if op == "lookup+":
+        return 9 + S * (1 + p2)
+    # insert / delete: key + result + bucket read(s) + one dirty-sector write-back
+    return 9 + S * (1 + p2) + 32
+
+
+def run_ours(args) -> None:
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    rank = int(os.environ.get("RANK", 0))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    from paper_2603_15486_b200 import CuckooFilter, FilterConfig, _lib
+    from paper_2603_15486_b200.sharded import ShardedCuckooFilter
+
+    log2 = args.log2_slots
+    f, b = 16, 16
+    m_local = (1 << log2) // b
+    n = int(0.95 * (1 << log2))  # keys per rank per op
+    S = 32 * ((b * f // 8 + 31) // 32)
+    cfg = FilterConfig(bucket_count=m_local * world, fingerprint_bits=f, bucket_slots=b,
+                       policy="xor", eviction=args.eviction, seed=0)
+
+    pos_h = gen_keys(n, rank)
+    neg_h = gen_keys(n, rank, negative=True)
+    pos = torch.from_numpy(pos_h.view(np.int64)).to(dev)
+    neg = torch.from_numpy(neg_h.view(np.int64)).to(dev)
+    if world > 1:
+        filt = ShardedCuckooFilter(cfg, device=dev)
+    else:
+        filt = CuckooFilter(cfg, device=dev)
+
+    stream = torch.cuda.current_stream(dev)
+    ops = ("insert", "lookup+", "lookup-", "delete")
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            dist.barrier()
+
+    def step(ev=None):
+        if ev:
+            ev[0].record(stream)
+        filt.insert_batch(pos)
+        if ev:
+            ev[1].record(stream)
+        filt.query_batch(pos)
+        if ev:
+            ev[2].record(stream)
+        filt.query_batch(neg)
+        if ev:
+            ev[3].record(stream)
+        filt.delete_batch(pos)
+        if ev:
+            ev[4].record(stream)
+
+    for _ in range(args.warmup):
+        step()
+    barrier()
+    events = [[torch.cuda.Event(enable_timing=True) for _ in range(5)] for _ in range(args.steps)]
+    launches0 = _lib.kernel_launches()
+    with ClockSampler(local) as clk:
+        barrier()
+        for k in range(args.steps):
+            step(events[k])
+        barrier()
+    launches = _lib.kernel_launches() - launches0
+    per_op = {o: 0.0 for o in ops}
+    for evs in events:
+        for j, o in enumerate(ops):
+            per_op[o] += evs[j].elapsed_time(evs[j + 1])
+    total_ms = sum(per_op.values())
+    ms_step = total_ms / args.steps
+    if world > 1:
+        t = torch.tensor([ms_step], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms_step = float(t.item())
+    value = 4 * n * world / (ms_step * 1e-3) / 1e9
+
+    # ---- verification pass (untimed): parity properties at full size ----
+    barrier()
+    res = filt.insert_batch(pos)
+    n_failed = res.n_failed
+    q_alt_ins = res.n_alt / n if hasattr(res, "n_alt") else None
+    hits = filt.query_batch(pos)
+    no_fn = bool(hits.all())
+    p2_pos = filt.last_counters()["n_alt"] / n
+    fpr = float(filt.query_batch(neg).float().mean())
+    d = filt.delete_batch(pos)
+    p2_del = filt.last_counters()["n_alt"] / n
+    all_deleted = bool(d.all())
+    occ_end = len(filt)
+    verify = {"insert_failures": int(n_failed), "no_false_negatives": no_fn, "fpr": fpr,
+              "all_deleted": all_deleted, "occupancy_after_delete": int(occ_end)}
+
+    peaks = measured_peaks()
+    p2 = {"insert": q_alt_ins or 0.0, "lookup+": p2_pos, "lookup-": 1.0, "delete": p2_del}
+    op_stats = {}
+    for o in ops:
+        t_s = per_op[o] / args.steps * 1e-3
+        gops = n / t_s / 1e9
+        bpo = alg_bytes(o, S, p2[o])
+        op_stats[o] = {"G_ops_s": round(gops, 3), "ms": round(per_op[o] / args.steps, 4),
+                       "bytes_per_op": round(bpo, 2), "p2": round(p2[o], 4),
+                       "achieved_GBs": round(gops * bpo, 1), "frac": round(gops * bpo / peaks["hbm_gbs"], 4)}
+    dom = max(ops, key=lambda o: per_op[o])
+    traffic = None
+    tf = ROOT / "profiles" / "traffic.json"
+    if tf.exists():
+        traffic = json.loads(tf.read_text()).get(dom)
+    roofline = {"bound": "hbm", "achieved": op_stats[dom]["achieved_GBs"], "peak": peaks["hbm_gbs"],
+                "unit": "GB/s", "frac": op_stats[dom]["frac"], "traffic": traffic,
+                "kernel": f"{dom} ({'insert_kernel+evict_kernel' if dom == 'insert' else dom.rstrip('+-') + '_kernel'})",
+                "peak_source": peaks["source"],
+                "random_sector_ceiling": "~48 G random 32B sectors/s at 512 MiB (profiles/r01_probe_ceiling.txt)"}
+
+    # ---- end to end through the public API with pinned host buffers ----
+    e2e = None
+    if not args.no_e2e:
+        pos_p = torch.from_numpy(pos_h.view(np.int64)).pin_memory()
+        neg_p = torch.from_numpy(neg_h.view(np.int64)).pin_memory()
+        del pos, neg
+        torch.cuda.empty_cache()
+
+        def e2e_step():
+            r = filt.insert_batch(pos_p)
+            ok_h = r.ok  # D2H of the per-key results
+            q1 = filt.query_batch(pos_p)
+            q2 = filt.query_batch(neg_p)
+            dd = filt.delete_batch(pos_p)
+            return ok_h, q1, q2, dd
+
+        e2e_step()
+        barrier()
+        t0 = time.perf_counter()
+        ksteps = max(1, min(args.steps, args.e2e_steps))
+        for _ in range(ksteps):
+            out = e2e_step()
+        barrier()
+        dt = (time.perf_counter() - t0) / ksteps
+        if world > 1:
+            t = torch.tensor([dt], device=dev, dtype=torch.float64)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            dt = float(t.item())
+        assert bool(out[1].all())
+        e2e = {"value": 4 * n * world / dt / 1e9, "unit": UNIT, "h2d_bytes_per_step": 4 * 8 * n,
+               "d2h_bytes_per_step": 4 * n, "ms_per_step": 1e3 * dt,
+               "path": "CuckooFilter.*_batch(pinned host torch tensors) -> host results"}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        import oracle
+
+        oracle.build()
+        th = host_threads()
+        r = cpu_protocol(args.cpu_log2_slots, pos_h, neg_h, th)
+        cpu = {"value": r["value"], "unit": UNIT, "cores": th, "kind": "port",
+               "sample": (f"oracle/ C restatement of the reference kernels; one step protocol on a "
+                          f"2^{args.cpu_log2_slots}-slot table (n={r['n']}), insert/delete 1 thread, "
+                          f"lookups {th} threads; {r['seconds']:.1f} s"),
+               "per_op_Mops": {k: round(v, 2) for k, v in r["per_op_Mops"].items()}}
+
+    if rank == 0:
+        line = {
+            "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "data": "synthetic (reference gen_keys Philox streams, seed = rank)",
+            "config": {"workload": "configs[1]: 2^28 slots/GPU f=16 b=16 xor, insert 0->95% then lookup+/-, delete",
+                       "slots_per_gpu": 1 << log2, "keys_per_op_per_gpu": n, "fingerprint_bits": f,
+                       "bucket_slots": b, "policy": "xor", "eviction": args.eviction,
+                       "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+                       "l2": "inputs > L2 (2 GiB key arrays, 512 MiB table vs 126 MB L2); no flush"},
+            "roofline": roofline, "ops": op_stats, "verify": verify,
+            "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
+            "clocks": clk.summary(),
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+def main() -> None:
+    ap = argparse.ArgumentParser(description=__doc__, formatter_class=argparse.RawDescriptionHelpFormatter)
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=5)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--log2-slots", type=int, default=28)
+    ap.add_argument("--eviction", choices=["dfs", "bfs"], default="bfs")
+    ap.add_argument("--cpu-log2-slots", type=int, default=24)
+    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

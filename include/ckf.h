@@ -91,11 +91,15 @@ typedef struct ckf_counters {
   unsigned long long n_ok;         /* successful inserts / deletes */
   unsigned long long n_records;    /* records produced (may exceed capacity) */
   unsigned long long n_queued;     /* keys that entered the eviction pass */
-  unsigned long long reserved;
+  unsigned long long n_alt;        /* keys that had to probe their alternate bucket
+                                      (insert: i1 full; query/delete: no match in i1) */
 } ckf_counters;
 
 int ckf_abi_version(void);
 const char* ckf_strerror(int code);
+/* Process-wide count of kernels this library has launched (evidence for the
+ * benchmark's gpu_launches field). */
+uint64_t ckf_kernel_launches(void);
 
 /* Validates like FilterConfig (placement.py:77-102) and derives geometry. */
 int ckf_params_init(ckf_params* p, uint64_t bucket_count, uint32_t fingerprint_bits,
@@ -119,9 +123,10 @@ int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                uint64_t record_cap, ckf_counters* counters, long long* occupancy,
                unsigned flags, void* stream);
 
-/* Batch membership; out[i] in {0,1}.  Read-only phase (filter.py:9-15). */
+/* Batch membership; out[i] in {0,1}.  Read-only phase (filter.py:9-15).
+ * counters (nullable) receives n_ok = hits and n_alt. */
 int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, uint64_t n,
-              uint8_t* out, unsigned flags, void* stream);
+              uint8_t* out, ckf_counters* counters, unsigned flags, void* stream);
 
 /* Batch delete; out[i] = 1 where a lane was cleared.  occupancy (nullable)
  * is atomically decreased by n_ok. */

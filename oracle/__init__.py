@@ -83,10 +83,12 @@ def lib():
         L.ck_alt.argtypes = [P(CkCfg), ctypes.c_uint64, ctypes.c_uint64, ctypes.c_uint64,
                              P(ctypes.c_uint64)]
         L.ck_insert_batch.restype = ctypes.c_int64
-        L.ck_insert_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, u64p, u64p]
+        L.ck_insert_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, u64p, u64p,
+                                      ctypes.c_int]
         L.ck_delete_batch.restype = ctypes.c_int64
-        L.ck_delete_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p]
-        L.ck_query_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int]
+        L.ck_delete_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int]
+        L.ck_query_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int,
+                                     ctypes.c_int]
         L.ck_try_insert.restype = ctypes.c_int64
         L.ck_try_insert.argtypes = [P(CkCfg), u64p, ctypes.c_int64, ctypes.c_uint64]
         L.ck_remove_tag.restype = ctypes.c_int64
@@ -159,29 +161,29 @@ class OracleFilter:
         self.words = np.zeros(int(cfg.m) * int(cfg.wpb), dtype=np.uint64)
         self.occupancy = 0
 
-    def insert_batch(self, keys):
+    def insert_batch(self, keys, hashed: bool = False):
         k = _keys(keys)
         n = len(k)
         ok = np.zeros(n, np.uint8)
         ev = np.zeros(n, np.int64)
         lost = np.zeros(n, np.uint64)
         n_ok = lib().ck_insert_batch(ctypes.byref(self.cfg), _ptr(self.words), _ptr(k), n,
-                                     _ptr(ok), _ptr(ev), _ptr(lost))
+                                     _ptr(ok), _ptr(ev), _ptr(lost), int(hashed))
         self.occupancy += int(n_ok)
         return ok.view(np.bool_), ev, lost
 
-    def query_batch(self, keys, threads: int = 1) -> np.ndarray:
+    def query_batch(self, keys, threads: int = 1, hashed: bool = False) -> np.ndarray:
         k = _keys(keys)
         out = np.zeros(len(k), np.uint8)
         lib().ck_query_batch(ctypes.byref(self.cfg), _ptr(self.words), _ptr(k), len(k),
-                             _ptr(out), threads)
+                             _ptr(out), threads, int(hashed))
         return out.view(np.bool_)
 
-    def delete_batch(self, keys) -> np.ndarray:
+    def delete_batch(self, keys, hashed: bool = False) -> np.ndarray:
         k = _keys(keys)
         out = np.zeros(len(k), np.uint8)
         n_ok = lib().ck_delete_batch(ctypes.byref(self.cfg), _ptr(self.words), _ptr(k), len(k),
-                                     _ptr(out))
+                                     _ptr(out), int(hashed))
         self.occupancy -= int(n_ok)
         return out.view(np.bool_)
 

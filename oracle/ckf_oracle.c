@@ -185,10 +185,11 @@ static int bucket_any_empty(const u64* words, i64 base, const ck_cfg* c) {
 /* ---------------- whole operations ---------------- */
 
 /* insert_one (K:331-436): direct placement, then DFS or BFS eviction.
- * Returns ok; *rounds and *lost as the reference reports them. */
-static int insert_key(u64* words, u64 key, const ck_cfg* c, i64* rounds, u64* lost,
-                      i64* cand_slot, u64* cand_tag) {
-  u64 h = ck_xxh64(key, c->seed), fp, i1, i2;
+ * Returns ok; *rounds and *lost as the reference reports them.  `h` is the
+ * key's xxh64 (K:355). */
+static int insert_hash(u64* words, u64 h, const ck_cfg* c, i64* rounds, u64* lost,
+                       i64* cand_slot, u64* cand_tag) {
+  u64 fp, i1, i2;
   place_hash(h, c, &fp, &i1, &i2);
   u64 tag1 = fp;
   u64 tag2 = make_tag(fp, c->policy == 1 ? 1u : 0u, c);
@@ -299,18 +300,18 @@ static int insert_key(u64* words, u64 key, const ck_cfg* c, i64* rounds, u64* lo
 }
 
 /* query_one (K:439-458): offset matches payload bits only (K:451-453). */
-static int query_key(const u64* words, u64 key, const ck_cfg* c) {
+static int query_hash(const u64* words, u64 h, const ck_cfg* c) {
   u64 ignore = c->policy == 1 ? c->high : 0u;
   u64 fp, i1, i2;
-  place_hash(ck_xxh64(key, c->seed), c, &fp, &i1, &i2);
+  place_hash(h, c, &fp, &i1, &i2);
   return bucket_has(words, (i64)i1 * c->wpb, fp, ignore, c) ||
          bucket_has(words, (i64)i2 * c->wpb, fp, ignore, c);
 }
 
 /* delete_one (K:461-484): full-lane match, i1 with fp then i2 with fp|choice. */
-static int delete_key(u64* words, u64 key, const ck_cfg* c) {
+static int delete_hash(u64* words, u64 h, const ck_cfg* c) {
   u64 fp, i1, i2;
-  place_hash(ck_xxh64(key, c->seed), c, &fp, &i1, &i2);
+  place_hash(h, c, &fp, &i1, &i2);
   u64 tag2 = c->policy == 1 ? make_tag(fp, 1u, c) : fp;
   if (bucket_take(words, (i64)i1 * c->wpb, fp, c) >= 0) return 1;
   return bucket_take(words, (i64)i2 * c->wpb, tag2, c) >= 0;
@@ -334,8 +335,12 @@ u64 ck_alt(const ck_cfg* c, u64 i, u64 fp, u64 choice, u64* new_choice) {
   return alt_bucket(i, fp, choice, c, new_choice);
 }
 
+static inline u64 key_hash(u64 k, const ck_cfg* c, int hashed) { return hashed ? k : ck_xxh64(k, c->seed); }
+
+/* `hashed` != 0: keys[] already holds xxh64(key, seed) (the multi-GPU router
+ * ships hashes so the owning shard skips the rehash). */
 i64 ck_insert_batch(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* ok,
-                    i64* evictions, u64* lost) {
+                    i64* evictions, u64* lost, int hashed) {
   i64 lim = (i64)c->b / 2;
   if (lim < 1) lim = 1;
   i64* cs = (i64*)malloc(sizeof(i64) * lim);
@@ -344,7 +349,7 @@ i64 ck_insert_batch(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t
   for (i64 i = 0; i < n; ++i) {
     i64 r;
     u64 l;
-    int good = insert_key(words, keys[i], c, &r, &l, cs, ct);
+    int good = insert_hash(words, key_hash(keys[i], c, hashed), c, &r, &l, cs, ct);
     if (ok) ok[i] = (uint8_t)good;
     if (evictions) evictions[i] = r;
     if (lost) lost[i] = l;
@@ -355,10 +360,10 @@ i64 ck_insert_batch(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t
   return n_ok;
 }
 
-i64 ck_delete_batch(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* out) {
+i64 ck_delete_batch(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* out, int hashed) {
   i64 n_ok = 0;
   for (i64 i = 0; i < n; ++i) {
-    int good = delete_key(words, keys[i], c);
+    int good = delete_hash(words, key_hash(keys[i], c, hashed), c);
     if (out) out[i] = (uint8_t)good;
     n_ok += good;
   }
@@ -371,25 +376,27 @@ typedef struct {
   const u64* keys;
   uint8_t* out;
   i64 lo, hi;
+  int hashed;
 } qjob;
 
 static void* query_worker(void* arg) {
   qjob* j = (qjob*)arg;
-  for (i64 i = j->lo; i < j->hi; ++i) j->out[i] = (uint8_t)query_key(j->words, j->keys[i], j->c);
+  for (i64 i = j->lo; i < j->hi; ++i)
+    j->out[i] = (uint8_t)query_hash(j->words, key_hash(j->keys[i], j->c, j->hashed), j->c);
   return NULL;
 }
 
 /* query_batch; threads > 1 splits contiguous chunks like filter.py:390-392. */
 void ck_query_batch(const ck_cfg* c, const u64* words, const u64* keys, i64 n, uint8_t* out,
-                    int threads) {
+                    int threads, int hashed) {
   if (threads <= 1 || n == 0) {
-    for (i64 i = 0; i < n; ++i) out[i] = (uint8_t)query_key(words, keys[i], c);
+    for (i64 i = 0; i < n; ++i) out[i] = (uint8_t)query_hash(words, key_hash(keys[i], c, hashed), c);
     return;
   }
   pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
   qjob* jobs = (qjob*)malloc(sizeof(qjob) * threads);
   for (int t = 0; t < threads; ++t) {
-    jobs[t] = (qjob){c, words, keys, out, (t * n) / threads, ((t + 1) * n) / threads};
+    jobs[t] = (qjob){c, words, keys, out, (t * n) / threads, ((t + 1) * n) / threads, hashed};
     pthread_create(&tid[t], NULL, query_worker, &jobs[t]);
   }
   for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);

@@ -63,12 +63,13 @@ _P = ctypes.POINTER(Params)
 SIGNATURES = {
     "ckf_abi_version": (ctypes.c_int, []),
     "ckf_strerror": (ctypes.c_char_p, [ctypes.c_int]),
+    "ckf_kernel_launches": (_u64, []),
     "ckf_params_init": (ctypes.c_int, [_P, _u64, _u32, _u32, ctypes.c_int, ctypes.c_int, _u32, _u64]),
     "ckf_hash": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "ckf_place": (ctypes.c_int, [_P, _vp, _u64, _vp, _vp, _vp, ctypes.c_uint, _vp]),
     "ckf_insert": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp, _vp,
                                   ctypes.c_uint, _vp]),
-    "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, ctypes.c_uint, _vp]),
+    "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
     "ckf_delete": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, ctypes.c_uint, _vp]),
     "ckf_host_hash": (_u64, [_u64, _u64]),
     "ckf_host_place": (None, [_P, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
@@ -103,6 +104,11 @@ def lib() -> ctypes.CDLL:
             raise ImportError(f"libckf ABI {L.ckf_abi_version()} != expected {ABI_VERSION}")
         _lib = L
     return _lib
+
+
+def kernel_launches() -> int:
+    """Kernels libckf.so has launched in this process (bench evidence)."""
+    return int(lib().ckf_kernel_launches())
 
 
 def check(rc: int) -> None:

@@ -24,6 +24,8 @@
 
 #include <stdint.h>
 
+#include <atomic>
+
 #include "../../include/ckf.h"
 #include "ckf_semantics.cuh"
 
@@ -361,17 +363,24 @@ __device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_
 // block-level counting: one global atomic per block
 // ---------------------------------------------------------------------------
 
-__device__ __forceinline__ void block_count_add(uint32_t mine, ckf_counters* ctr, long long* occ, int sign) {
-  __shared__ unsigned int s_sum;
-  if (threadIdx.x == 0) s_sum = 0;
+__device__ __forceinline__ void block_count_add(uint32_t mine, uint32_t alt, ckf_counters* ctr, long long* occ,
+                                                int sign) {
+  __shared__ unsigned int s_sum[2];
+  if (threadIdx.x < 2) s_sum[threadIdx.x] = 0;
   __syncthreads();
   unsigned int w = __reduce_add_sync(0xffffffffu, mine);
-  if ((threadIdx.x & 31) == 0 && w) atomicAdd(&s_sum, w);
+  unsigned int wa = __reduce_add_sync(0xffffffffu, alt);
+  if ((threadIdx.x & 31) == 0) {
+    if (w) atomicAdd(&s_sum[0], w);
+    if (wa) atomicAdd(&s_sum[1], wa);
+  }
   __syncthreads();
-  if (threadIdx.x == 0 && s_sum) {
-    if (ctr) atomicAdd(&ctr->n_ok, (unsigned long long)s_sum);
-    if (occ) atomicAdd(reinterpret_cast<unsigned long long*>(occ),
-                       (unsigned long long)((long long)sign * (long long)s_sum));
+  if (threadIdx.x == 0) {
+    if (ctr && s_sum[0]) atomicAdd(&ctr->n_ok, (unsigned long long)s_sum[0]);
+    if (ctr && s_sum[1]) atomicAdd(&ctr->n_alt, (unsigned long long)s_sum[1]);
+    if (occ && s_sum[0])
+      atomicAdd(reinterpret_cast<unsigned long long*>(occ),
+                (unsigned long long)((long long)sign * (long long)s_sum[0]));
   }
 }
 
@@ -411,9 +420,10 @@ __global__ void __launch_bounds__(kBlock) hash_kernel(const uint64_t* __restrict
 template <int F, int WPB, int POL, int KPT>
 __global__ void __launch_bounds__(kBlock) query_kernel(Geo g, const uint64_t* __restrict__ words,
                                                        const uint64_t* __restrict__ keys, uint64_t n,
-                                                       uint8_t* __restrict__ out, bool hashed) {
+                                                       uint8_t* __restrict__ out, ckf_counters* ctr, bool hashed) {
   using L = Lanes<F>;
   constexpr int W = WPB > 0 ? WPB : 1;
+  uint32_t n_hit = 0, n_alt = 0;
   const uint64_t keep = POL == CKF_POLICY_OFFSET ? ~L::kHigh : ~0ull;
   const uint64_t tile = (uint64_t)kBlock * KPT;
   for (uint64_t t0 = blockIdx.x * tile; t0 < n; t0 += (uint64_t)gridDim.x * tile) {
@@ -441,8 +451,12 @@ __global__ void __launch_bounds__(kBlock) query_kernel(Geo g, const uint64_t* __
         hit[k] = any != 0;
       }
 #pragma unroll
-      for (int k = 0; k < KPT; ++k)
-        if (valid[k] && !hit[k]) ld_bucket_ro<WPB>(words + i2[k] * WPB, w[k]);
+      for (int k = 0; k < KPT; ++k) {
+        if (valid[k] && !hit[k]) {
+          ++n_alt;
+          ld_bucket_ro<WPB>(words + i2[k] * WPB, w[k]);
+        }
+      }
 #pragma unroll
       for (int k = 0; k < KPT; ++k) {
         if (hit[k]) continue;
@@ -459,6 +473,7 @@ __global__ void __launch_bounds__(kBlock) query_kernel(Geo g, const uint64_t* __
         if (!valid[k]) continue;
         const uint64_t pat = L::bcast(fp[k]);
         for (int pass = 0; pass < 2 && !hit[k]; ++pass) {
+          n_alt += pass;
           const uint64_t* p = words + (pass ? i2[k] : i1[k]) * g.wpb;
           for (uint32_t j = 0; j < g.wpb; ++j)
             if (L::zeros((__ldg(p + j) & keep) ^ pat)) {
@@ -469,9 +484,12 @@ __global__ void __launch_bounds__(kBlock) query_kernel(Geo g, const uint64_t* __
       }
     }
 #pragma unroll
-    for (int k = 0; k < KPT; ++k)
+    for (int k = 0; k < KPT; ++k) {
       if (valid[k]) out[t0 + k * kBlock + threadIdx.x] = hit[k] ? 1 : 0;
+      n_hit += valid[k] && hit[k];
+    }
   }
+  if (ctr) block_count_add(n_hit, n_alt, ctr, nullptr, +1);
 }
 
 // Insert, direct pass (K:355-362): TryInsert(i1, fp) then TryInsert(i2, fp|choice).
@@ -484,7 +502,7 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
                                                         uint64_t* __restrict__ lost, ckf_record* __restrict__ rec,
                                                         uint64_t cap, ckf_counters* ctr, long long* occ,
                                                         bool hashed) {
-  uint32_t n_ok = 0;
+  uint32_t n_ok = 0, n_alt = 0;
   const int lane_id = threadIdx.x & 31;
   for (uint64_t t0 = blockIdx.x * (uint64_t)kBlock; t0 < n; t0 += (uint64_t)gridDim.x * kBlock) {
     const uint64_t i = t0 + threadIdx.x;
@@ -495,7 +513,10 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
       h = load_hash(keys, i, g.seed, hashed);
       place<POL>(h, g, fp, i1, i2);
       bool done = try_insert_any<F, WPB>(words, i1, fp, g) >= 0;
-      if (!done) done = try_insert_any<F, WPB>(words, i2, make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g), g) >= 0;
+      if (!done) {
+        ++n_alt;
+        done = try_insert_any<F, WPB>(words, i2, make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g), g) >= 0;
+      }
       need = !done;
       n_ok += done;
       ok[i] = done ? 1 : 0;
@@ -522,7 +543,7 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
       }
     }
   }
-  block_count_add(n_ok, ctr, occ, +1);
+  block_count_add(n_ok, n_alt, ctr, occ, +1);
 }
 
 // Eviction pass over the queued keys (the ~4% whose pair was full at 95% load).
@@ -547,7 +568,7 @@ __global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restri
     if (lost) lost[i] = o.lost;
   }
   if (threadIdx.x == 0 && blockIdx.x == 0) ctr->n_records = cnt;
-  block_count_add(n_ok, ctr, occ, +1);
+  block_count_add(n_ok, 0, ctr, occ, +1);
 }
 
 // Delete (K:461-484): full-lane match, i1 with fp, then i2 with fp|choice.
@@ -556,17 +577,19 @@ __global__ void __launch_bounds__(kBlock) delete_kernel(Geo g, uint64_t* __restr
                                                         const uint64_t* __restrict__ keys, uint64_t n,
                                                         uint8_t* __restrict__ out, ckf_counters* ctr, long long* occ,
                                                         bool hashed) {
-  uint32_t n_ok = 0;
+  uint32_t n_ok = 0, n_alt = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t fp, i1, i2;
     place<POL>(load_hash(keys, i, g.seed, hashed), g, fp, i1, i2);
     bool done = remove_tag_any<F, WPB>(words, i1, fp, g) >= 0;
-    if (!done)
+    if (!done) {
+      ++n_alt;
       done = remove_tag_any<F, WPB>(words, i2, POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp, g) >= 0;
+    }
     out[i] = done ? 1 : 0;
     n_ok += done;
   }
-  block_count_add(n_ok, ctr, occ, -1);
+  block_count_add(n_ok, n_alt, ctr, occ, -1);
 }
 
 // Parity mode: the reference's sequential insert_batch (K:510-529), one
@@ -639,7 +662,16 @@ static unsigned grid_for(uint64_t work, uint64_t per_block, int blocks_per_sm) {
   return (unsigned)(need < cap ? need : cap);
 }
 
+static std::atomic<uint64_t> g_launches{0};
+
+static int cuda_error() {
+  cudaError_t e = cudaGetLastError();
+  return e == cudaSuccess ? CKF_OK : CKF_ECUDA_BASE - (int)e;
+}
+
+// Called right after every kernel launch: counts it and maps the error code.
 static int status() {
+  g_launches.fetch_add(1, std::memory_order_relaxed);
   cudaError_t e = cudaGetLastError();
   return e == cudaSuccess ? CKF_OK : CKF_ECUDA_BASE - (int)e;
 }
@@ -678,6 +710,7 @@ struct QueryArgs {
   const uint64_t* keys;
   uint64_t n;
   uint8_t* out;
+  ckf_counters* ctr;
   bool hashed;
   cudaStream_t s;
 };
@@ -687,7 +720,7 @@ struct QueryOp {
   static int run(const QueryArgs& a) {
     constexpr int KPT = WPB >= 8 ? 1 : (WPB > 0 ? 2 : 1);
     unsigned grid = grid_for(a.n, (uint64_t)kBlock * KPT, 16);
-    query_kernel<F, WPB, POL, KPT><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.hashed);
+    query_kernel<F, WPB, POL, KPT><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.hashed);
     return status();
   }
 };
@@ -727,8 +760,9 @@ struct InsertOp {
       // strides over it (empty queues exit immediately)
       unsigned egrid = (unsigned)sm_count() * 4;
       evict_kernel<F, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ);
+      st = status();
     }
-    return status();
+    return st;
   }
 };
 
@@ -785,6 +819,8 @@ using namespace ckf;
 extern "C" {
 
 int ckf_abi_version(void) { return CKF_ABI_VERSION; }
+
+uint64_t ckf_kernel_launches(void) { return g_launches.load(std::memory_order_relaxed); }
 
 const char* ckf_strerror(int code) {
   if (code == CKF_OK) return "ok";
@@ -846,7 +882,7 @@ int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                unsigned flags, void* stream) {
   if (!params_ok(p) || !words || !counters) return CKF_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return status();
+  if (cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !ok || (record_cap && !records)) return CKF_EINVAL;
   InsertArgs a{geo_from(*p), words, keys, n, ok, evictions, lost, records, records ? record_cap : 0,
@@ -855,11 +891,13 @@ int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
 }
 
 int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* out,
-              unsigned flags, void* stream) {
+              ckf_counters* counters, unsigned flags, void* stream) {
   if (!params_ok(p) || !words) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (counters && cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
-  QueryArgs a{geo_from(*p), words, keys, n, out, (flags & CKF_INPUT_HASHED) != 0, (cudaStream_t)stream};
+  QueryArgs a{geo_from(*p), words, keys, n, out, counters, (flags & CKF_INPUT_HASHED) != 0, s};
   return dispatch3<QueryOp>(p, words, a);
 }
 
@@ -867,7 +905,7 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                ckf_counters* counters, long long* occupancy, unsigned flags, void* stream) {
   if (!params_ok(p) || !words) return CKF_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
-  if (counters && cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return status();
+  if (counters && cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,

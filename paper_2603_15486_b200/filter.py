@@ -103,12 +103,13 @@ class BatchInsertResult:
     """
 
     def __init__(self, n: int, ok_dev: torch.Tensor, records: torch.Tensor, counters: torch.Tensor,
-                 as_numpy: bool):
+                 kind: str):
         self._n = n
         self._ok_dev = ok_dev
         self._rec = records
         self._ctr = counters
-        self._numpy = as_numpy
+        self._kind = kind
+        self._numpy = kind == "numpy"
         self._ok = None
         self._ev = None
         self._lost = None
@@ -120,7 +121,14 @@ class BatchInsertResult:
             c = self._ctr.cpu()
             self._nok_cached = int(c[0])
             self._nrec = int(c[1])
+            self._nalt = int(c[3])
         return self._nok_cached, self._nrec
+
+    @property
+    def n_alt(self) -> int:
+        """Keys whose primary bucket was full (they probed the alternate)."""
+        self._counts()
+        return self._nalt
 
     @property
     def n_ok(self) -> int:
@@ -139,8 +147,7 @@ class BatchInsertResult:
     @property
     def ok(self):
         if self._ok is None:
-            okb = self._ok_dev.view(torch.bool)
-            self._ok = okb.cpu().numpy() if self._numpy else okb
+            self._ok = CuckooFilter._answer(self._ok_dev.view(torch.bool), self._kind)
         return self._ok
 
     def _expand(self):
@@ -154,9 +161,9 @@ class BatchInsertResult:
         if self._numpy:
             self._ev, self._lost = ev, lost
         else:
-            dev = self._ok_dev.device
+            dev = self._ok_dev.device if self._kind == "cuda" else "cpu"
             self._ev = torch.from_numpy(ev).to(dev)
-            self._lost = torch.from_numpy(lost.view(np.int64)).to(dev)
+            self._lost = torch.from_numpy(lost).to(dev)
 
     @property
     def evictions(self):
@@ -274,7 +281,9 @@ class CuckooFilter:
         return torch.cuda.current_stream(self.device).cuda_stream
 
     def _as_keys(self, keys):
-        """Contiguous device int64 view of the keys + whether to answer in numpy."""
+        """Contiguous device int64 view of the keys + where answers should go:
+        "numpy" (host arrays / sequences, like the reference), "cpu" (a host
+        torch tensor; pinned memory gives an async DMA) or "cuda" (stay on device)."""
         if isinstance(keys, torch.Tensor):
             if keys.dim() != 1:
                 raise ValueError("keys must be one-dimensional")
@@ -282,14 +291,27 @@ class CuckooFilter:
                 keys = keys.view(torch.int64)
             elif keys.dtype != torch.int64:
                 keys = keys.to(torch.int64)
+            if keys.device.type == "cpu":
+                return keys.contiguous().to(self.device, non_blocking=True), "cpu"
             if keys.device != self.device:
-                return keys.to(self.device, non_blocking=True).contiguous(), False
-            return keys.contiguous(), False
+                return keys.to(self.device, non_blocking=True).contiguous(), "cuda"
+            return keys.contiguous(), "cuda"
         arr = np.ascontiguousarray(keys, dtype=np.uint64)
         if arr.ndim != 1:
             raise ValueError("keys must be one-dimensional")
         t = torch.from_numpy(arr.view(np.int64))
-        return t.to(self.device), True
+        return t.to(self.device), "numpy"
+
+    @staticmethod
+    def _answer(dev_bool: torch.Tensor, kind: str):
+        if kind == "cuda":
+            return dev_bool
+        if kind == "cpu":
+            host = torch.empty(dev_bool.shape, dtype=torch.bool, pin_memory=True)
+            host.copy_(dev_bool, non_blocking=True)
+            torch.cuda.current_stream(dev_bool.device).synchronize()
+            return host
+        return dev_bool.cpu().numpy()
 
     def _flags(self, deterministic: Optional[bool]) -> int:
         det = self._deterministic if deterministic is None else deterministic
@@ -339,38 +361,42 @@ class CuckooFilter:
 
     # ---- batch operations ----
 
-    def insert_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None) -> BatchInsertResult:
-        """Insert every key; results are index-aligned with the input (filter.py:401-442)."""
+    def insert_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None,
+                     hashed: bool = False) -> BatchInsertResult:
+        """Insert every key; results are index-aligned with the input (filter.py:401-442).
+
+        ``hashed=True``: the values are xxh64(key, seed) already (multi-GPU router)."""
         if self._debug:
             self._enter_mutate()
         try:
-            return self._insert(keys, 0, deterministic)
+            return self._insert(keys, 0, deterministic, hashed)
         finally:
             if self._debug:
                 self._exit_mutate()
 
-    def query_batch(self, keys, workers: int = 1):
+    def query_batch(self, keys, workers: int = 1, *, hashed: bool = False):
         """Boolean membership per key (filter.py:444-473)."""
         if self._debug:
             self._enter_read()
         try:
-            return self._query(keys)
+            return self._query(keys, hashed)
         finally:
             if self._debug:
                 self._exit_read()
 
-    def delete_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None):
+    def delete_batch(self, keys, workers: int = 1, *, deterministic: Optional[bool] = None,
+                     hashed: bool = False):
         """Delete each key once; True where a matching lane was cleared (filter.py:475-502)."""
         if self._debug:
             self._enter_mutate()
         try:
-            return self._delete(keys, deterministic)
+            return self._delete(keys, deterministic, hashed)
         finally:
             if self._debug:
                 self._exit_mutate()
 
-    def _insert(self, keys, worker: int, deterministic: Optional[bool]) -> BatchInsertResult:
-        k, as_np = self._as_keys(keys)
+    def _insert(self, keys, worker: int, deterministic: Optional[bool], hashed: bool = False) -> BatchInsertResult:
+        k, kind = self._as_keys(keys)
         n = k.numel()
         with torch.cuda.device(self.device):
             ok = torch.empty(n, dtype=torch.uint8, device=self.device)
@@ -380,31 +406,34 @@ class CuckooFilter:
             _lib.check(_lib.lib().ckf_insert(
                 ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, ok.data_ptr(),
                 None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(),
-                self._flags(deterministic), self._stream()))
-        return BatchInsertResult(n, ok, rec, ctr, as_np)
+                self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0), self._stream()))
+        return BatchInsertResult(n, ok, rec, ctr, kind)
 
-    def _query(self, keys):
-        k, as_np = self._as_keys(keys)
+    def _query(self, keys, hashed: bool = False):
+        k, kind = self._as_keys(keys)
         n = k.numel()
         with torch.cuda.device(self.device):
             out = torch.empty(n, dtype=torch.uint8, device=self.device)
             _lib.check(_lib.lib().ckf_query(
                 ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
-                out.data_ptr(), 0, self._stream()))
-        res = out.view(torch.bool)
-        return res.cpu().numpy() if as_np else res
+                out.data_ptr(), self._ctr.data_ptr(), _lib.INPUT_HASHED if hashed else 0, self._stream()))
+        return self._answer(out.view(torch.bool), kind)
 
-    def _delete(self, keys, deterministic: Optional[bool]):
-        k, as_np = self._as_keys(keys)
+    def _delete(self, keys, deterministic: Optional[bool], hashed: bool = False):
+        k, kind = self._as_keys(keys)
         n = k.numel()
         with torch.cuda.device(self.device):
             out = torch.empty(n, dtype=torch.uint8, device=self.device)
             _lib.check(_lib.lib().ckf_delete(
                 ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
                 out.data_ptr(), self._ctr.data_ptr(), self._occ.data_ptr(),
-                self._flags(deterministic), self._stream()))
-        res = out.view(torch.bool)
-        return res.cpu().numpy() if as_np else res
+                self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0), self._stream()))
+        return self._answer(out.view(torch.bool), kind)
+
+    def last_counters(self) -> dict:
+        """Device counters of the last query / delete batch (one small D2H)."""
+        c = self._ctr.cpu().tolist()
+        return {"n_ok": c[0], "n_alt": c[3]}
 
     def collect_eviction_stats(self, keys, prefill_fraction: float = 0.75, workers: int = 1) -> EvictionStats:
         """Insert all keys, sampling eviction counts past the prefill (filter.py:504-519)."""

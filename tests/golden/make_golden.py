@@ -128,7 +128,7 @@ def main() -> None:
         out[f"{name}_dres"] = filt.delete_batch(dels).astype(np.uint8)
         out[f"{name}_words_del"] = filt.words.copy()
         out[f"{name}_qafter"] = filt.query_batch(ins).astype(np.uint8)
-        out[f"{name}_blobhdr"] = np.frombuffer(filt.to_bytes()[:40], dtype=np.uint8)
+        out[f"{name}_blobhdr"] = np.frombuffer(filt.to_bytes()[:44], dtype=np.uint8)
         manifest["scenarios"].append({
             "name": name, "m": m, "f": f, "b": b, "policy": pol, "eviction": ev,
             "max_evictions": max_ev, "seed": seed, "load": load, "n": n,

@@ -86,7 +86,7 @@ def test_null_and_empty_calls_are_rejected_or_noops():
     L = _lib.lib()
     p = FilterConfig(bucket_count=64).ckf_params()
     # missing table pointer
-    assert L.ckf_query(ctypes.byref(p), None, None, 0, None, 0, None) == _lib.EINVAL
+    assert L.ckf_query(ctypes.byref(p), None, None, 0, None, None, 0, None) == _lib.EINVAL
     assert L.ckf_hash(None, 0, 0, None, None) == 0  # n == 0 is a no-op
 
 

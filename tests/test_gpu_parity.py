@@ -96,7 +96,7 @@ def test_parity_mode_is_bit_identical(sc):
     assert np.array_equal(dres.astype(np.uint8), DATA[f"{name}_dres"])
     assert np.array_equal(filt.words, DATA[f"{name}_words_del"])
     assert filt.occupancy == sc["occ_after_delete"]
-    hdr = filt.to_bytes()[:40]
+    hdr = filt.to_bytes()[:44]
     assert hdr == bytes(DATA[f"{name}_blobhdr"]), "CKGF header differs from the reference dump"
 
 
