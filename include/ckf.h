@@ -52,6 +52,13 @@ extern "C" {
 #define CKF_MODE_SEQUENTIAL 1u   /* one device thread, reference key order:
                                     bit-identical to insert_batch(workers=1) */
 #define CKF_INPUT_HASHED 2u      /* `keys` already holds xxh64(key, seed) */
+#define CKF_FORCE_DIRECT 4u      /* never use the L2-tiled path */
+#define CKF_FORCE_TILED 8u       /* use the L2-tiled path whenever it applies */
+
+/* op ids for ckf_workspace_bytes */
+#define CKF_OP_QUERY 0
+#define CKF_OP_INSERT 1
+#define CKF_OP_DELETE 2
 
 /* Filter geometry: the reference `_kargs` tuple (filter.py:150-154) plus the
  * eviction knobs; filled and validated by ckf_params_init. Passed by pointer,
@@ -113,6 +120,12 @@ int ckf_hash(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, voi
 int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* fp, uint64_t* i1,
               uint64_t* i2, unsigned flags, void* stream);
 
+/* Scratch bytes for which a batch of n keys runs L2-tiled (binned by bucket
+ * region so every random bucket access is served from L2).
+ * 0 means this batch runs on the direct kernels and needs no workspace.
+ * Passing a smaller (or NULL) workspace to an op also selects the direct path. */
+uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags);
+
 /* Batch insert.  ok[n] is required.  evictions/lost are optional DENSE
  * outputs with the reference's types (int64 / uint64 per key).  records
  * (capacity record_cap) receives the sparse outcomes and doubles as the
@@ -121,18 +134,19 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
 int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n,
                uint8_t* ok, int64_t* evictions, uint64_t* lost, ckf_record* records,
                uint64_t record_cap, ckf_counters* counters, long long* occupancy,
-               unsigned flags, void* stream);
+               void* workspace, uint64_t workspace_bytes, unsigned flags, void* stream);
 
 /* Batch membership; out[i] in {0,1}.  Read-only phase (filter.py:9-15).
  * counters (nullable) receives n_ok = hits and n_alt. */
 int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, uint64_t n,
-              uint8_t* out, ckf_counters* counters, unsigned flags, void* stream);
+              uint8_t* out, ckf_counters* counters, void* workspace, uint64_t workspace_bytes,
+              unsigned flags, void* stream);
 
 /* Batch delete; out[i] = 1 where a lane was cleared.  occupancy (nullable)
  * is atomically decreased by n_ok. */
 int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n,
-               uint8_t* out, ckf_counters* counters, long long* occupancy, unsigned flags,
-               void* stream);
+               uint8_t* out, ckf_counters* counters, long long* occupancy, void* workspace,
+               uint64_t workspace_bytes, unsigned flags, void* stream);
 
 /* Host-compiled copies of the shared device semantics (same source as the
  * kernels); used by derive_placement() and by the CPU parity tests. */

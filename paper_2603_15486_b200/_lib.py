@@ -28,6 +28,12 @@ EVICT_BFS = 1
 MODE_CONCURRENT = 0
 MODE_SEQUENTIAL = 1
 INPUT_HASHED = 2
+FORCE_DIRECT = 4
+FORCE_TILED = 8
+
+OP_QUERY = 0
+OP_INSERT = 1
+OP_DELETE = 2
 
 
 class Params(ctypes.Structure):
@@ -67,10 +73,12 @@ SIGNATURES = {
     "ckf_params_init": (ctypes.c_int, [_P, _u64, _u32, _u32, ctypes.c_int, ctypes.c_int, _u32, _u64]),
     "ckf_hash": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "ckf_place": (ctypes.c_int, [_P, _vp, _u64, _vp, _vp, _vp, ctypes.c_uint, _vp]),
+    "ckf_workspace_bytes": (_u64, [_P, _u64, ctypes.c_int, ctypes.c_uint]),
     "ckf_insert": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp, _vp,
-                                  ctypes.c_uint, _vp]),
-    "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
-    "ckf_delete": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, ctypes.c_uint, _vp]),
+                                  _vp, _u64, ctypes.c_uint, _vp]),
+    "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.c_uint, _vp]),
+    "ckf_delete": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, ctypes.c_uint,
+                                  _vp]),
     "ckf_host_hash": (_u64, [_u64, _u64]),
     "ckf_host_place": (None, [_P, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
                               ctypes.POINTER(_u64)]),

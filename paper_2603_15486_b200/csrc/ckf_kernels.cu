@@ -25,369 +25,14 @@
 #include <stdint.h>
 
 #include <atomic>
+#include <cmath>
 
 #include "../../include/ckf.h"
 #include "ckf_semantics.cuh"
+#include "ckf_device.cuh"
+#include "ckf_tiled.cuh"
 
 namespace ckf {
-
-constexpr int kMaxSlots = 128;  // GPU limit on bucket_slots (BFS candidate scratch)
-
-// ---------------------------------------------------------------------------
-// memory primitives
-// ---------------------------------------------------------------------------
-
-// Streaming key read: read-only path, no L1 allocation.
-__device__ __forceinline__ uint64_t ld_stream(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(v) : "l"(p));
-  return v;
-}
-
-// Read-only bucket fetch (query phase only): one 256-bit
-// ld.global.nc per 32-byte sector.
-template <int WPB>
-__device__ __forceinline__ void ld_bucket_ro(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
-  if constexpr (WPB == 1) {
-    asm volatile("ld.global.nc.L1::no_allocate.u64 %0, [%1];" : "=l"(w[0]) : "l"(p));
-  } else if constexpr (WPB == 2) {
-    asm volatile("ld.global.nc.L1::no_allocate.v2.u64 {%0,%1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p));
-  } else if constexpr (WPB >= 4) {
-#pragma unroll
-    for (int s = 0; s < WPB / 4; ++s)
-      asm volatile("ld.global.nc.L1::no_allocate.v4.u64 {%0,%1,%2,%3}, [%4];"
-                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
-                   : "l"(p + 4 * s));
-  }
-}
-
-// Coherent bucket snapshot for the mutating kernels: relaxed gpu-scope loads
-// are served by L2 (where the CAS commits), never a stale L1 line.
-template <int WPB>
-__device__ __forceinline__ void ld_bucket_rw(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
-  if constexpr (WPB == 1) {
-    asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(w[0]) : "l"(p) : "memory");
-  } else if constexpr (WPB == 2) {
-    asm volatile("ld.relaxed.gpu.global.v2.u64 {%0,%1}, [%2];" : "=l"(w[0]), "=l"(w[1]) : "l"(p) : "memory");
-  } else if constexpr (WPB >= 4) {
-#pragma unroll
-    for (int s = 0; s < WPB / 4; ++s)
-      asm volatile("ld.relaxed.gpu.global.v4.u64 {%0,%1,%2,%3}, [%4];"
-                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
-                   : "l"(p + 4 * s)
-                   : "memory");
-  }
-}
-
-__device__ __forceinline__ uint64_t ld_word_rw(const uint64_t* p) {
-  uint64_t v;
-  asm volatile("ld.relaxed.gpu.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
-  return v;
-}
-
-__device__ __forceinline__ uint64_t cas64(uint64_t* p, uint64_t expect, uint64_t desired) {
-  return atomicCAS(reinterpret_cast<unsigned long long*>(p), (unsigned long long)expect,
-                   (unsigned long long)desired);
-}
-
-// ---------------------------------------------------------------------------
-// bucket operations
-// ---------------------------------------------------------------------------
-
-// TryInsert (K:158-180): lowest empty lane of the first word,
-// in wrap order from (tag % b)/tpw, that has one; committed by CAS, rescanning
-// the word the CAS lost on.  Returns the slot or -1.  Compile-time WPB.
-template <int F, int WPB>
-__device__ __forceinline__ int try_insert_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
-  using L = Lanes<F>;
-  constexpr int kB = WPB * L::kTpw;
-  uint64_t* base = words + bucket * WPB;
-  uint64_t w[WPB];
-  ld_bucket_rw<WPB>(base, w);
-  const int start = (int)(tag % kB) / L::kTpw;
-  while (true) {
-    int best = -1, bestp = WPB;
-    uint64_t bw = 0;
-#pragma unroll
-    for (int j = 0; j < WPB; ++j) {
-      int pos = (j - start + WPB) % WPB;  // scan position of word j
-      if (L::zeros(w[j]) && pos < bestp) {
-        best = j;
-        bestp = pos;
-        bw = w[j];
-      }
-    }
-    if (best < 0) return -1;
-    int lane = L::first(L::zeros(bw));
-    uint64_t old = cas64(base + best, bw, L::put(bw, lane, tag));
-    if (old == bw) return best * L::kTpw + lane;
-#pragma unroll
-    for (int j = 0; j < WPB; ++j)
-      if (j == best) w[j] = old;
-  }
-}
-
-// Same contract, runtime words-per-bucket (any legal b).
-template <int F>
-__device__ int try_insert_rt(uint64_t* words, uint64_t bucket, uint64_t tag, const Geo& g) {
-  using L = Lanes<F>;
-  uint64_t* base = words + bucket * g.wpb;
-  const uint32_t start = (uint32_t)(tag % g.b) / L::kTpw;
-  for (uint32_t k = 0; k < g.wpb; ++k) {
-    uint32_t wi = start + k;
-    if (wi >= g.wpb) wi -= g.wpb;
-    uint64_t w = ld_word_rw(base + wi);
-    while (true) {
-      uint64_t z = L::zeros(w);
-      if (!z) break;
-      int lane = L::first(z);
-      uint64_t old = cas64(base + wi, w, L::put(w, lane, tag));
-      if (old == w) return (int)(wi * L::kTpw) + lane;
-      w = old;
-    }
-  }
-  return -1;
-}
-
-// TryRemove (K:202-221): CAS-clear the first lane, in scan
-// order, equal to `tag` (full-lane match).  Returns the slot or -1.
-template <int F, int WPB>
-__device__ __forceinline__ int remove_tag_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
-  using L = Lanes<F>;
-  constexpr int kB = WPB * L::kTpw;
-  uint64_t* base = words + bucket * WPB;
-  uint64_t w[WPB];
-  ld_bucket_rw<WPB>(base, w);
-  const uint64_t pat = L::bcast(tag);
-  const int start = (int)(tag % kB) / L::kTpw;
-  while (true) {
-    int best = -1, bestp = WPB;
-    uint64_t bw = 0;
-#pragma unroll
-    for (int j = 0; j < WPB; ++j) {
-      int pos = (j - start + WPB) % WPB;
-      if (L::zeros(w[j] ^ pat) && pos < bestp) {
-        best = j;
-        bestp = pos;
-        bw = w[j];
-      }
-    }
-    if (best < 0) return -1;
-    int lane = L::first(L::zeros(bw ^ pat));
-    uint64_t old = cas64(base + best, bw, L::put(bw, lane, 0));
-    if (old == bw) return best * L::kTpw + lane;
-#pragma unroll
-    for (int j = 0; j < WPB; ++j)
-      if (j == best) w[j] = old;
-  }
-}
-
-template <int F>
-__device__ int remove_tag_rt(uint64_t* words, uint64_t bucket, uint64_t tag, const Geo& g) {
-  using L = Lanes<F>;
-  uint64_t* base = words + bucket * g.wpb;
-  const uint64_t pat = L::bcast(tag);
-  const uint32_t start = (uint32_t)(tag % g.b) / L::kTpw;
-  for (uint32_t k = 0; k < g.wpb; ++k) {
-    uint32_t wi = start + k;
-    if (wi >= g.wpb) wi -= g.wpb;
-    uint64_t w = ld_word_rw(base + wi);
-    while (true) {
-      uint64_t mm = L::zeros(w ^ pat);
-      if (!mm) break;
-      int lane = L::first(mm);
-      uint64_t old = cas64(base + wi, w, L::put(w, lane, 0));
-      if (old == w) return (int)(wi * L::kTpw) + lane;
-      w = old;
-    }
-  }
-  return -1;
-}
-
-template <int F, int WPB>
-__device__ __forceinline__ int try_insert_any(uint64_t* words, uint64_t bucket, uint64_t tag, const Geo& g) {
-  if constexpr (WPB > 0) return try_insert_t<F, WPB>(words, bucket, tag);
-  else return try_insert_rt<F>(words, bucket, tag, g);
-}
-template <int F, int WPB>
-__device__ __forceinline__ int remove_tag_any(uint64_t* words, uint64_t bucket, uint64_t tag, const Geo& g) {
-  if constexpr (WPB > 0) return remove_tag_t<F, WPB>(words, bucket, tag);
-  else return remove_tag_rt<F>(words, bucket, tag, g);
-}
-
-// Atomic lane exchange (swap_slot, K:232-244).
-template <int F>
-__device__ uint64_t swap_slot(uint64_t* words, uint64_t bucket, uint32_t slot, uint64_t tag, const Geo& g) {
-  using L = Lanes<F>;
-  uint64_t* p = words + bucket * g.wpb + slot / L::kTpw;
-  const int lane = slot % L::kTpw;
-  uint64_t w = ld_word_rw(p);
-  while (true) {
-    uint64_t old = cas64(p, w, L::put(w, lane, tag));
-    if (old == w) return L::get(w, lane);
-    w = old;
-  }
-}
-
-// Replace a lane only while it still holds `expect` (lane_cas, K:247-254);
-// unrelated lanes of the word may change underneath and are retried.
-template <int F>
-__device__ bool lane_cas(uint64_t* p, int lane, uint64_t expect, uint64_t repl) {
-  using L = Lanes<F>;
-  uint64_t w = ld_word_rw(p);
-  while (true) {
-    if (L::get(w, lane) != expect) return false;
-    uint64_t old = cas64(p, w, L::put(w, lane, repl));
-    if (old == w) return true;
-    w = old;
-  }
-}
-
-template <int F>
-__device__ bool bucket_has_empty(const uint64_t* words, uint64_t bucket, const Geo& g) {
-  const uint64_t* p = words + bucket * g.wpb;
-  for (uint32_t k = 0; k < g.wpb; ++k)
-    if (Lanes<F>::zeros(ld_word_rw(p + k))) return true;
-  return false;
-}
-
-// ---------------------------------------------------------------------------
-// eviction chain (insert_one after both direct attempts failed, K:364-436)
-// ---------------------------------------------------------------------------
-
-struct Outcome {
-  uint32_t ok;
-  uint32_t rounds;
-  uint64_t lost;
-};
-
-template <int F, int POL>
-__device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2,
-                               const Geo& g) {
-  using L = Lanes<F>;
-  const uint64_t tag1 = fp;
-  const uint64_t tag2 = make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g);
-  uint64_t st = rng_init(g.seed, h, g.worker) + kGolden;
-  uint64_t cur_b, cur_tag;
-  if ((smix(st) & 1u) == 0) {
-    cur_b = i1;
-    cur_tag = tag1;
-  } else {
-    cur_b = i2;
-    cur_tag = tag2;
-  }
-  const uint64_t b = g.b;
-
-  if (g.eviction == CKF_EVICT_DFS) {  // K:374-389
-    for (uint32_t n = 1; n <= g.max_evictions; ++n) {
-      st += kGolden;
-      uint32_t victim = (uint32_t)(smix(st) % b);
-      uint64_t ev = swap_slot<F>(words, cur_b, victim, cur_tag, g);
-      if (ev == 0) return {1u, n, 0};  // a concurrent delete freed the lane
-      uint64_t nc;
-      uint64_t efp = tag_fp(ev, g);
-      cur_b = alt_index<POL>(cur_b, efp, tag_choice(ev, g), g, nc);
-      cur_tag = make_tag(efp, nc, g);
-      if (try_insert_rt<F>(words, cur_b, cur_tag, g) >= 0) return {1u, n, 0};
-    }
-    return {0u, g.max_evictions, tag_fp(cur_tag, g)};
-  }
-
-  // BFS (K:391-436): probe up to b/2 occupied candidates for a free alternate
-  const uint32_t limit = g.b / 2 ? g.b / 2 : 1;
-  uint32_t cslot[kMaxSlots / 2];
-  uint64_t ctag[kMaxSlots / 2];
-  for (uint32_t n = 1; n <= g.max_evictions; ++n) {
-    st += kGolden;
-    const uint32_t start = (uint32_t)(smix(st) % b);
-    uint64_t* base = words + cur_b * g.wpb;
-    // collect_candidates (K:257-272): snapshot, occupied lanes from `start`, wrapping
-    uint32_t cnt = 0;
-    uint64_t w = 0;
-    uint32_t wcur = ~0u;
-    for (uint32_t j = 0; j < g.b && cnt < limit; ++j) {
-      uint32_t s = start + j;
-      if (s >= g.b) s -= g.b;
-      uint32_t wi = s / L::kTpw;
-      if (wi != wcur) {
-        w = ld_word_rw(base + wi);
-        wcur = wi;
-      }
-      uint64_t t = L::get(w, s % L::kTpw);
-      if (t) {
-        cslot[cnt] = s;
-        ctag[cnt] = t;
-        ++cnt;
-      }
-    }
-    if (cnt == 0) {  // drained by concurrent deletes: take a direct slot
-      if (try_insert_rt<F>(words, cur_b, cur_tag, g) >= 0) return {1u, n, 0};
-      continue;
-    }
-    int chosen = -1;
-    uint64_t alt_b = 0, alt_tag = 0;
-    for (uint32_t j = 0; j < cnt; ++j) {
-      uint64_t tc;
-      uint64_t cfp = tag_fp(ctag[j], g);
-      uint64_t tb = alt_index<POL>(cur_b, cfp, tag_choice(ctag[j], g), g, tc);
-      if (bucket_has_empty<F>(words, tb, g)) {
-        chosen = (int)j;
-        alt_b = tb;
-        alt_tag = make_tag(cfp, tc, g);
-        break;
-      }
-    }
-    if (chosen >= 0) {
-      // two-step relocation: copy the candidate out, then swap ourselves in
-      int aslot = try_insert_rt<F>(words, alt_b, alt_tag, g);
-      if (aslot < 0) continue;  // the free lane raced away
-      uint32_t os = cslot[chosen];
-      if (lane_cas<F>(base + os / L::kTpw, os % L::kTpw, ctag[chosen], cur_tag)) return {1u, n, 0};
-      // origin lane changed underfoot: remove the copy we just made
-      lane_cas<F>(words + alt_b * g.wpb + aslot / L::kTpw, aslot % L::kTpw, alt_tag, 0);
-      continue;
-    }
-    // nobody has room: evict the last candidate and deepen (K:427-434)
-    uint32_t os = cslot[cnt - 1];
-    uint64_t ct = ctag[cnt - 1];
-    if (!lane_cas<F>(base + os / L::kTpw, os % L::kTpw, ct, cur_tag)) continue;
-    uint64_t nc;
-    uint64_t cfp = tag_fp(ct, g);
-    cur_b = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, nc);
-    cur_tag = make_tag(cfp, nc, g);
-  }
-  return {0u, g.max_evictions, tag_fp(cur_tag, g)};
-}
-
-// ---------------------------------------------------------------------------
-// block-level counting: one global atomic per block
-// ---------------------------------------------------------------------------
-
-__device__ __forceinline__ void block_count_add(uint32_t mine, uint32_t alt, ckf_counters* ctr, long long* occ,
-                                                int sign) {
-  __shared__ unsigned int s_sum[2];
-  if (threadIdx.x < 2) s_sum[threadIdx.x] = 0;
-  __syncthreads();
-  unsigned int w = __reduce_add_sync(0xffffffffu, mine);
-  unsigned int wa = __reduce_add_sync(0xffffffffu, alt);
-  if ((threadIdx.x & 31) == 0) {
-    if (w) atomicAdd(&s_sum[0], w);
-    if (wa) atomicAdd(&s_sum[1], wa);
-  }
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    if (ctr && s_sum[0]) atomicAdd(&ctr->n_ok, (unsigned long long)s_sum[0]);
-    if (ctr && s_sum[1]) atomicAdd(&ctr->n_alt, (unsigned long long)s_sum[1]);
-    if (occ && s_sum[0])
-      atomicAdd(reinterpret_cast<unsigned long long*>(occ),
-                (unsigned long long)((long long)sign * (long long)s_sum[0]));
-  }
-}
-
-__device__ __forceinline__ uint64_t load_hash(const uint64_t* keys, uint64_t i, uint64_t seed, bool hashed) {
-  uint64_t k = ld_stream(keys + i);
-  return hashed ? k : xxh64(k, seed);
-}
 
 // ---------------------------------------------------------------------------
 // kernels
@@ -704,6 +349,120 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
   return CKF_EINVAL;
 }
 
+
+// ---------------------------------------------------------------------------
+// L2-tiled execution: plan + workspace layout (host side; see ckf_tiled.cuh)
+// ---------------------------------------------------------------------------
+
+constexpr uint64_t kRegionBytes = 2ull << 20;   // table bytes per bin (L2 working set per bin)
+constexpr uint64_t kTiledMinTable = 48ull << 20; // below this the table is L2-resident anyway
+
+struct Layout {
+  uint64_t cnt1, cnt2, h1, x1, h2, x2, bits, total;
+};
+
+static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
+
+static bool tiled_applies(const ckf_params* p, uint64_t n, unsigned flags) {
+  if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
+  const uint32_t wpb = p->words_per_bucket;
+  if (wpb != 2 && wpb != 4 && wpb != 8) return false;
+  if (p->bucket_count > 0xFFFFFFFFull || n >= 0xFFFFFFFFull || n == 0) return false;
+  if (flags & CKF_FORCE_TILED) return true;
+  const uint64_t table = p->bucket_count * wpb * 8ull;
+  // enough keys per bucket that binning turns re-fetches into L2 hits
+  return table >= kTiledMinTable && n >= p->bucket_count;
+}
+
+static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags) {
+  const uint64_t m = p->bucket_count;
+  const uint64_t table = m * p->words_per_bucket * 8ull;
+  uint64_t region = (flags & CKF_FORCE_TILED) && table < 64 * kRegionBytes ? (table / 64 ? table / 64 : 1) : kRegionBytes;
+  uint64_t want = table / region;
+  uint32_t R = 1;
+  while ((uint64_t)R * 2 <= want && R * 2 <= (uint32_t)kMaxBins) R *= 2;
+  const bool pow2 = (m & (m - 1)) == 0;
+  if (pow2)
+    while (R > m) R /= 2;
+  Plan pl{};
+  pl.R = R;
+  pl.pow2 = pow2;
+  if (pow2) {
+    uint32_t lm = 0, lr = 0;
+    while ((1ull << lm) < m) ++lm;
+    while ((1u << lr) < R) ++lr;
+    pl.shift = lm - lr;
+  } else {
+    pl.magic = (uint64_t)(((unsigned __int128)R << 32) / m);
+  }
+  const double per = (double)((n + R - 1) / R);
+  uint64_t cap = (uint64_t)(per + 4.0 * std::sqrt(per) + 64.0);
+  cap = (cap + kTile - 1) / kTile * kTile;
+  pl.cap = cap;
+  pl.tiles_per_bin = (uint32_t)(cap / kTile);
+  return pl;
+}
+
+static Layout layout_for(const Plan& pl, uint64_t n, int op) {
+  Layout L{};
+  L.cnt1 = 0;
+  L.cnt2 = kMaxBins * 4;
+  uint64_t off = align256(2 * kMaxBins * 4);
+  const uint64_t recs = (uint64_t)pl.R * pl.cap;
+  L.h1 = off;
+  off = align256(off + recs * 8);
+  L.x1 = off;
+  off = align256(off + recs * 4);
+  L.h2 = off;
+  off = align256(off + recs * 8);
+  L.x2 = off;
+  off = align256(off + recs * 4);
+  L.bits = off;
+  if (op != CKF_OP_INSERT) off = align256(off + (n + 31) / 32 * 4);
+  L.total = off;
+  return L;
+}
+
+static Work work_view(void* ws, const Layout& L) {
+  char* b = (char*)ws;
+  return Work{(uint32_t*)(b + L.cnt1), (uint32_t*)(b + L.cnt2), (uint64_t*)(b + L.h1), (uint32_t*)(b + L.x1),
+              (uint64_t*)(b + L.h2),   (uint32_t*)(b + L.x2),   (uint32_t*)(b + L.bits)};
+}
+
+// Tiled run of one op: memsets + pass A/B/C (+ bit expansion for query/delete).
+template <int OP, int F, int WPB, int POL>
+static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, uint64_t* words, const uint64_t* keys,
+                     uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out, cudaStream_t s) {
+  Work w = work_view(ws, L);
+  if (cudaMemsetAsync(ws, 0, 2 * kMaxBins * 4, s) != cudaSuccess) return cuda_error();
+  if (OP != OP_INSERT) {
+    if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
+    sk.bits = w.bits;
+  }
+  const unsigned gbin = grid_for(n, kTile, 4);
+  tile_bin_kernel<OP, F, WPB, POL><<<gbin, kTileThreads, 0, s>>>(g, pl, words, keys, n, hashed, w, sk, occ);
+  int st = status();
+  if (st) return st;
+  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
+  const unsigned gt = (unsigned)(tiles < 0x7FFFFFFFull ? tiles : 0x7FFFFFFFull);
+  tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
+  if ((st = status())) return st;
+  tile_probe2_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
+  if ((st = status())) return st;
+  if (OP != OP_INSERT) {
+    expand_bits_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out);
+    st = status();
+  }
+  return st;
+}
+
+struct TiledArgs {
+  bool on;
+  Plan pl;
+  Layout L;
+  void* ws;
+};
+
 struct QueryArgs {
   Geo g;
   const uint64_t* words;
@@ -713,11 +472,19 @@ struct QueryArgs {
   ckf_counters* ctr;
   bool hashed;
   cudaStream_t s;
+  TiledArgs t;
 };
 
 template <int F, int WPB, int POL>
 struct QueryOp {
   static int run(const QueryArgs& a) {
+    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+      if (a.t.on) {
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, nullptr};
+        return run_tiled<OP_QUERY, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
+                                                a.n, a.hashed, sk, nullptr, a.out, a.s);
+      }
+    }
     constexpr int KPT = WPB >= 8 ? 1 : (WPB > 0 ? 2 : 1);
     unsigned grid = grid_for(a.n, (uint64_t)kBlock * KPT, 16);
     query_kernel<F, WPB, POL, KPT><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.hashed);
@@ -740,6 +507,7 @@ struct InsertArgs {
   bool hashed;
   bool sequential;
   cudaStream_t s;
+  TiledArgs t;
 };
 
 template <int F, int WPB, int POL>
@@ -750,11 +518,28 @@ struct InsertOp {
                                                    a.occ, a.hashed);
       return status();
     }
-    unsigned grid = grid_for(a.n, kBlock, 16);
-    insert_kernel<F, WPB, POL><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec, a.cap,
-                                                         a.ctr, a.occ, a.hashed);
-    int st = status();
-    if (st) return st;
+    int st = CKF_OK;
+    bool tiled = false;
+    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+      if (a.t.on && a.cap) {
+        tiled = true;
+        // every key counts as stored until the eviction pass says otherwise
+        if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
+        if (a.ev && cudaMemsetAsync(a.ev, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
+        if (a.lost && cudaMemsetAsync(a.lost, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
+        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, a.ev, a.lost};
+        st = run_tiled<OP_INSERT, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk, a.occ,
+                                               nullptr, a.s);
+        if (st) return st;
+      }
+    }
+    if (!tiled) {
+      unsigned grid = grid_for(a.n, kBlock, 16);
+      insert_kernel<F, WPB, POL><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec,
+                                                           a.cap, a.ctr, a.occ, a.hashed);
+      st = status();
+      if (st) return st;
+    }
     if (a.cap) {
       // the queue length is only known on the device: a fixed full-residency grid
       // strides over it (empty queues exit immediately)
@@ -777,6 +562,7 @@ struct DeleteArgs {
   bool hashed;
   bool sequential;
   cudaStream_t s;
+  TiledArgs t;
 };
 
 template <int F, int WPB, int POL>
@@ -785,6 +571,13 @@ struct DeleteOp {
     if (a.sequential) {
       seq_delete_kernel<F, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.occ, a.hashed);
       return status();
+    }
+    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+      if (a.t.on) {
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, nullptr};
+        return run_tiled<OP_DELETE, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
+                                                 a.occ, a.out, a.s);
+      }
     }
     unsigned grid = grid_for(a.n, kBlock, 16);
     delete_kernel<F, WPB, POL><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.occ, a.hashed);
@@ -877,39 +670,59 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
                             (cudaStream_t)stream);
 }
 
+// Decide tiled vs direct for one call: tiled needs the plan to apply and a
+// large enough caller workspace.
+static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, void* ws, uint64_t ws_bytes) {
+  TiledArgs t{};
+  if (!ws || !tiled_applies(p, n, flags)) return t;
+  t.pl = make_plan(p, n, flags);
+  t.L = layout_for(t.pl, n, op);
+  t.ws = ws;
+  t.on = ws_bytes >= t.L.total && ((uintptr_t)ws % 256) == 0;
+  return t;
+}
+
+uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
+  if (!params_ok(p) || !tiled_applies(p, n, flags)) return 0;
+  return layout_for(make_plan(p, n, flags), n, op).total;
+}
+
 int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* ok, int64_t* evictions,
                uint64_t* lost, ckf_record* records, uint64_t record_cap, ckf_counters* counters, long long* occupancy,
-               unsigned flags, void* stream) {
+               void* workspace, uint64_t workspace_bytes, unsigned flags, void* stream) {
   if (!params_ok(p) || !words || !counters) return CKF_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   if (cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !ok || (record_cap && !records)) return CKF_EINVAL;
   InsertArgs a{geo_from(*p), words, keys, n, ok, evictions, lost, records, records ? record_cap : 0,
-               counters, occupancy, (flags & CKF_INPUT_HASHED) != 0, (flags & CKF_MODE_SEQUENTIAL) != 0, s};
+               counters, occupancy, (flags & CKF_INPUT_HASHED) != 0, (flags & CKF_MODE_SEQUENTIAL) != 0, s,
+               choose(p, n, CKF_OP_INSERT, flags, workspace, workspace_bytes)};
   return dispatch3<InsertOp>(p, words, a);
 }
 
 int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* out,
-              ckf_counters* counters, unsigned flags, void* stream) {
+              ckf_counters* counters, void* workspace, uint64_t workspace_bytes, unsigned flags, void* stream) {
   if (!params_ok(p) || !words) return CKF_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   if (counters && cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
-  QueryArgs a{geo_from(*p), words, keys, n, out, counters, (flags & CKF_INPUT_HASHED) != 0, s};
+  QueryArgs a{geo_from(*p), words, keys, n, out, counters, (flags & CKF_INPUT_HASHED) != 0, s,
+              choose(p, n, CKF_OP_QUERY, flags, workspace, workspace_bytes)};
   return dispatch3<QueryOp>(p, words, a);
 }
 
 int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* out,
-               ckf_counters* counters, long long* occupancy, unsigned flags, void* stream) {
+               ckf_counters* counters, long long* occupancy, void* workspace, uint64_t workspace_bytes, unsigned flags,
+               void* stream) {
   if (!params_ok(p) || !words) return CKF_EINVAL;
   cudaStream_t s = (cudaStream_t)stream;
   if (counters && cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,
-               (flags & CKF_MODE_SEQUENTIAL) != 0, s};
+               (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, workspace, workspace_bytes)};
   return dispatch3<DeleteOp>(p, words, a);
 }
 

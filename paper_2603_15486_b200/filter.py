@@ -198,13 +198,16 @@ class CuckooFilter:
     """
 
     def __init__(self, cfg: FilterConfig, *, debug_phase: bool = False, device=None,
-                 deterministic: bool = False):
+                 deterministic: bool = False, tiled: Optional[bool] = None):
         self.cfg = cfg
         self.device = torch.device(device) if device is not None else _default_device()
         if self.device.type != "cuda":
             raise RuntimeError("CuckooFilter runs on CUDA devices only")
         self._params = cfg.ckf_params()
         self._deterministic = deterministic
+        # None: library heuristic; True: L2-tiled whenever applicable; False: direct kernels
+        self._tiled_flags = {None: 0, True: _lib.FORCE_TILED, False: _lib.FORCE_DIRECT}[tiled]
+        self._ws = None  # grow-only scratch for the L2-tiled path
         with torch.cuda.device(self.device):
             self.words_device = torch.zeros(cfg.total_words, dtype=torch.int64, device=self.device)
             # [0] occupancy (kernels add/subtract), [1..4] scratch counters for scalar ops
@@ -315,7 +318,17 @@ class CuckooFilter:
 
     def _flags(self, deterministic: Optional[bool]) -> int:
         det = self._deterministic if deterministic is None else deterministic
-        return _lib.MODE_SEQUENTIAL if det else _lib.MODE_CONCURRENT
+        return (_lib.MODE_SEQUENTIAL if det else _lib.MODE_CONCURRENT) | self._tiled_flags
+
+    def _workspace(self, p, n: int, op: int, flags: int):
+        """(pointer, bytes) of scratch for an L2-tiled run, or (None, 0)."""
+        need = int(_lib.lib().ckf_workspace_bytes(ctypes.byref(p), n, op, flags))
+        if need == 0:
+            return None, 0
+        if self._ws is None or self._ws.numel() < need:
+            self._ws = None
+            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return self._ws.data_ptr(), self._ws.numel()
 
     def _params_for(self, worker: int):
         if worker == 0:
@@ -403,10 +416,12 @@ class CuckooFilter:
             rec = torch.empty(max(n, 1) * _lib.RECORD_BYTES, dtype=torch.uint8, device=self.device)
             ctr = torch.empty(4, dtype=torch.int64, device=self.device)
             p = self._params_for(worker)
+            flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
+            ws, wsb = self._workspace(p, n, _lib.OP_INSERT, flags)
             _lib.check(_lib.lib().ckf_insert(
                 ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, ok.data_ptr(),
-                None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(),
-                self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0), self._stream()))
+                None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(), ws, wsb,
+                flags, self._stream()))
         return BatchInsertResult(n, ok, rec, ctr, kind)
 
     def _query(self, keys, hashed: bool = False):
@@ -414,9 +429,11 @@ class CuckooFilter:
         n = k.numel()
         with torch.cuda.device(self.device):
             out = torch.empty(n, dtype=torch.uint8, device=self.device)
+            flags = self._tiled_flags | (_lib.INPUT_HASHED if hashed else 0)
+            ws, wsb = self._workspace(self._params, n, _lib.OP_QUERY, flags)
             _lib.check(_lib.lib().ckf_query(
                 ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
-                out.data_ptr(), self._ctr.data_ptr(), _lib.INPUT_HASHED if hashed else 0, self._stream()))
+                out.data_ptr(), self._ctr.data_ptr(), ws, wsb, flags, self._stream()))
         return self._answer(out.view(torch.bool), kind)
 
     def _delete(self, keys, deterministic: Optional[bool], hashed: bool = False):
@@ -424,10 +441,12 @@ class CuckooFilter:
         n = k.numel()
         with torch.cuda.device(self.device):
             out = torch.empty(n, dtype=torch.uint8, device=self.device)
+            flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
+            ws, wsb = self._workspace(self._params, n, _lib.OP_DELETE, flags)
             _lib.check(_lib.lib().ckf_delete(
                 ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
-                out.data_ptr(), self._ctr.data_ptr(), self._occ.data_ptr(),
-                self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0), self._stream()))
+                out.data_ptr(), self._ctr.data_ptr(), self._occ.data_ptr(), ws, wsb, flags,
+                self._stream()))
         return self._answer(out.view(torch.bool), kind)
 
     def last_counters(self) -> dict:

@@ -86,8 +86,24 @@ def test_null_and_empty_calls_are_rejected_or_noops():
     L = _lib.lib()
     p = FilterConfig(bucket_count=64).ckf_params()
     # missing table pointer
-    assert L.ckf_query(ctypes.byref(p), None, None, 0, None, None, 0, None) == _lib.EINVAL
+    assert L.ckf_query(ctypes.byref(p), None, None, 0, None, None, None, 0, 0, None) == _lib.EINVAL
     assert L.ckf_hash(None, 0, 0, None, None) == 0  # n == 0 is a no-op
+
+
+def test_workspace_sizing():
+    L = _lib.lib()
+    big = FilterConfig(bucket_count=1 << 24).ckf_params()
+    n = int(0.95 * (1 << 28))
+    wq = L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_QUERY, 0)
+    wi = L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_INSERT, 0)
+    # two binned copies of (8 B hash + 4 B index) per key (+ bitmap for query)
+    assert 24 * n <= wi < 25 * n and wq == wi + ((n + 31) // 32 * 4 + 255) // 256 * 256
+    small = FilterConfig(bucket_count=1 << 10).ckf_params()
+    assert L.ckf_workspace_bytes(ctypes.byref(small), 100_000, _lib.OP_QUERY, 0) == 0  # L2-resident
+    assert L.ckf_workspace_bytes(ctypes.byref(small), 100_000, _lib.OP_QUERY, _lib.FORCE_TILED) > 0
+    assert L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_QUERY, _lib.FORCE_DIRECT) == 0
+    b4 = FilterConfig(bucket_count=1 << 24, bucket_slots=4).ckf_params()  # 8-byte buckets: direct only
+    assert L.ckf_workspace_bytes(ctypes.byref(b4), n, _lib.OP_QUERY, _lib.FORCE_TILED) == 0
 
 
 def test_host_hash_matches_xxhash_package():
