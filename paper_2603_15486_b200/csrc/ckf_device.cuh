@@ -79,12 +79,10 @@ __device__ __forceinline__ uint64_t cas64(uint64_t* p, uint64_t expect, uint64_t
 // in wrap order from (tag % b)/tpw, that has one; committed by CAS, rescanning
 // the word the CAS lost on.  Returns the slot or -1.  Compile-time WPB.
 template <int F, int WPB>
-__device__ __forceinline__ int try_insert_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
+__device__ __forceinline__ int try_insert_snap(uint64_t* words, uint64_t bucket, uint64_t tag, uint64_t (&w)[WPB]) {
   using L = Lanes<F>;
   constexpr int kB = WPB * L::kTpw;
   uint64_t* base = words + bucket * WPB;
-  uint64_t w[WPB];
-  ld_bucket_rw<WPB>(base, w);
   const int start = (int)(tag % kB) / L::kTpw;
   while (true) {
     int best = -1, bestp = WPB;
@@ -106,6 +104,13 @@ __device__ __forceinline__ int try_insert_t(uint64_t* words, uint64_t bucket, ui
     for (int j = 0; j < WPB; ++j)
       if (j == best) w[j] = old;
   }
+}
+
+template <int F, int WPB>
+__device__ __forceinline__ int try_insert_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
+  uint64_t w[WPB];
+  ld_bucket_rw<WPB>(words + bucket * WPB, w);
+  return try_insert_snap<F, WPB>(words, bucket, tag, w);
 }
 
 // Same contract, runtime words-per-bucket (any legal b).
@@ -133,12 +138,10 @@ __device__ int try_insert_rt(uint64_t* words, uint64_t bucket, uint64_t tag, con
 // TryRemove (K:202-221): CAS-clear the first lane, in scan
 // order, equal to `tag` (full-lane match).  Returns the slot or -1.
 template <int F, int WPB>
-__device__ __forceinline__ int remove_tag_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
+__device__ __forceinline__ int remove_tag_snap(uint64_t* words, uint64_t bucket, uint64_t tag, uint64_t (&w)[WPB]) {
   using L = Lanes<F>;
   constexpr int kB = WPB * L::kTpw;
   uint64_t* base = words + bucket * WPB;
-  uint64_t w[WPB];
-  ld_bucket_rw<WPB>(base, w);
   const uint64_t pat = L::bcast(tag);
   const int start = (int)(tag % kB) / L::kTpw;
   while (true) {
@@ -161,6 +164,13 @@ __device__ __forceinline__ int remove_tag_t(uint64_t* words, uint64_t bucket, ui
     for (int j = 0; j < WPB; ++j)
       if (j == best) w[j] = old;
   }
+}
+
+template <int F, int WPB>
+__device__ __forceinline__ int remove_tag_t(uint64_t* words, uint64_t bucket, uint64_t tag) {
+  uint64_t w[WPB];
+  ld_bucket_rw<WPB>(words + bucket * WPB, w);
+  return remove_tag_snap<F, WPB>(words, bucket, tag, w);
 }
 
 template <int F>

@@ -26,6 +26,7 @@
 
 #include <atomic>
 #include <cmath>
+#include <cstdlib>
 
 #include "../../include/ckf.h"
 #include "ckf_semantics.cuh"
@@ -354,69 +355,86 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
 // L2-tiled execution: plan + workspace layout (host side; see ckf_tiled.cuh)
 // ---------------------------------------------------------------------------
 
-constexpr uint64_t kRegionBytes = 2ull << 20;   // table bytes per bin (L2 working set per bin)
+constexpr uint64_t kRegionBytes = 2ull << 20;   // table bytes per bin
 constexpr uint64_t kTiledMinTable = 48ull << 20; // below this the table is L2-resident anyway
 
 struct Layout {
-  uint64_t cnt1, cnt2, h1, x1, h2, x2, bits, total;
+  uint64_t cnt1, cnt2, bin1, bin2, bits, total;
 };
 
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
+
+// Developer knobs for sweeps (tools/sweep_tiled.py): CKF_REGION_KB, CKF_BIN_GROUP,
+// CKF_TILED_AUTO (0 disables the automatic choice of the tiled path).
+static uint64_t env_u64(const char* name, uint64_t dflt) {
+  const char* v = getenv(name);
+  return v && *v ? strtoull(v, nullptr, 10) : dflt;
+}
+
+// Binning plan; ok=false when the batch cannot be tiled.
+static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags, bool& ok) {
+  Plan pl{};
+  ok = false;
+  const uint64_t m = p->bucket_count;
+  const uint64_t bucket_bytes = p->words_per_bucket * 8ull;
+  const uint64_t table = m * bucket_bytes;
+  const bool forced = (flags & CKF_FORCE_TILED) != 0;
+  const uint64_t region_pref = env_u64("CKF_REGION_KB", kRegionBytes >> 10) << 10;
+  // small forced tables still get ~64 bins so the multi-bin logic is exercised
+  const uint64_t region = forced && table < 64 * region_pref ? (table / 64 ? table / 64 : 1) : region_pref;
+  uint64_t rb = region / bucket_bytes;
+  if (rb < 2) rb = 2;
+  const uint64_t max_rb = 1ull << (32 - p->payload_bits);  // bucket offset bits in a record
+  if (rb > max_rb) rb = max_rb;
+  uint64_t R = (m + rb - 1) / rb;
+  if (R > (uint64_t)kMaxBins) {
+    R = kMaxBins;
+    rb = (m + R - 1) / R;
+    if (rb > max_rb) return pl;
+  }
+  rb = (m + R - 1) / R;  // balance the regions
+  R = (m + rb - 1) / rb;
+  if (rb < 2) return pl;
+  pl.rb = (uint32_t)rb;
+  pl.R = (uint32_t)R;
+  pl.pb = p->payload_bits;
+  pl.div_magic = ~0ull / rb + 1;  // Lemire fastdiv: exact bucket / rb for bucket < 2^32
+  pl.group = (uint32_t)env_u64("CKF_BIN_GROUP", 8);
+  if (pl.group < 1) pl.group = 1;
+  const double per = (double)n / (double)R;
+  pl.cap = (uint64_t)(per + 4.0 * std::sqrt(per) + 64.0);
+  pl.tiles_per_bin = (uint32_t)((pl.cap + kTile - 1) / kTile);
+  ok = true;
+  return pl;
+}
 
 static bool tiled_applies(const ckf_params* p, uint64_t n, unsigned flags) {
   if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
   const uint32_t wpb = p->words_per_bucket;
   if (wpb != 2 && wpb != 4 && wpb != 8) return false;
-  if (p->bucket_count > 0xFFFFFFFFull || n >= 0xFFFFFFFFull || n == 0) return false;
-  if (flags & CKF_FORCE_TILED) return true;
-  const uint64_t table = p->bucket_count * wpb * 8ull;
-  // enough keys per bucket that binning turns re-fetches into L2 hits
-  return table >= kTiledMinTable && n >= p->bucket_count;
-}
-
-static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags) {
-  const uint64_t m = p->bucket_count;
-  const uint64_t table = m * p->words_per_bucket * 8ull;
-  uint64_t region = (flags & CKF_FORCE_TILED) && table < 64 * kRegionBytes ? (table / 64 ? table / 64 : 1) : kRegionBytes;
-  uint64_t want = table / region;
-  uint32_t R = 1;
-  while ((uint64_t)R * 2 <= want && R * 2 <= (uint32_t)kMaxBins) R *= 2;
-  const bool pow2 = (m & (m - 1)) == 0;
-  if (pow2)
-    while (R > m) R /= 2;
-  Plan pl{};
-  pl.R = R;
-  pl.pow2 = pow2;
-  if (pow2) {
-    uint32_t lm = 0, lr = 0;
-    while ((1ull << lm) < m) ++lm;
-    while ((1u << lr) < R) ++lr;
-    pl.shift = lm - lr;
-  } else {
-    pl.magic = (uint64_t)(((unsigned __int128)R << 32) / m);
+  if (p->bucket_count > 0xFFFFFFFFull || p->bucket_count < 64 || n >= 0xFFFFFFFFull || n == 0) return false;
+  if (p->payload_bits > 24) return false;  // record = idx:32 | offset | fp
+  if (!(flags & CKF_FORCE_TILED)) {
+    if (!env_u64("CKF_TILED_AUTO", 1)) return false;
+    const uint64_t table = p->bucket_count * wpb * 8ull;
+    // enough keys per bucket that binning turns re-fetches into L2 hits
+    if (table < kTiledMinTable || n < p->bucket_count) return false;
   }
-  const double per = (double)((n + R - 1) / R);
-  uint64_t cap = (uint64_t)(per + 4.0 * std::sqrt(per) + 64.0);
-  cap = (cap + kTile - 1) / kTile * kTile;
-  pl.cap = cap;
-  pl.tiles_per_bin = (uint32_t)(cap / kTile);
-  return pl;
+  bool ok;
+  make_plan(p, n, flags, ok);
+  return ok;
 }
 
 static Layout layout_for(const Plan& pl, uint64_t n, int op) {
   Layout L{};
   L.cnt1 = 0;
-  L.cnt2 = kMaxBins * 4;
-  uint64_t off = align256(2 * kMaxBins * 4);
+  L.cnt2 = align256((uint64_t)pl.R * kCntStride * 4);
+  uint64_t off = 2 * L.cnt2;
   const uint64_t recs = (uint64_t)pl.R * pl.cap;
-  L.h1 = off;
+  L.bin1 = off;
   off = align256(off + recs * 8);
-  L.x1 = off;
-  off = align256(off + recs * 4);
-  L.h2 = off;
+  L.bin2 = off;
   off = align256(off + recs * 8);
-  L.x2 = off;
-  off = align256(off + recs * 4);
   L.bits = off;
   if (op != CKF_OP_INSERT) off = align256(off + (n + 31) / 32 * 4);
   L.total = off;
@@ -425,26 +443,28 @@ static Layout layout_for(const Plan& pl, uint64_t n, int op) {
 
 static Work work_view(void* ws, const Layout& L) {
   char* b = (char*)ws;
-  return Work{(uint32_t*)(b + L.cnt1), (uint32_t*)(b + L.cnt2), (uint64_t*)(b + L.h1), (uint32_t*)(b + L.x1),
-              (uint64_t*)(b + L.h2),   (uint32_t*)(b + L.x2),   (uint32_t*)(b + L.bits)};
+  return Work{(uint32_t*)(b + L.cnt1), (uint32_t*)(b + L.cnt2), (uint64_t*)(b + L.bin1), (uint64_t*)(b + L.bin2),
+              (uint32_t*)(b + L.bits)};
 }
 
-// Tiled run of one op: memsets + pass A/B/C (+ bit expansion for query/delete).
+// Tiled run of one op: pass A/B/C (+ bit expansion for query/delete).
 template <int OP, int F, int WPB, int POL>
 static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, uint64_t* words, const uint64_t* keys,
                      uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out, cudaStream_t s) {
   Work w = work_view(ws, L);
-  if (cudaMemsetAsync(ws, 0, 2 * kMaxBins * 4, s) != cudaSuccess) return cuda_error();
+  if (cudaMemsetAsync(ws, 0, L.bin1, s) != cudaSuccess) return cuda_error();  // bin counters
   if (OP != OP_INSERT) {
     if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
     sk.bits = w.bits;
   }
-  const unsigned gbin = grid_for(n, kTile, 4);
-  tile_bin_kernel<OP, F, WPB, POL><<<gbin, kTileThreads, 0, s>>>(g, pl, words, keys, n, hashed, w, sk, occ);
+  sk.keys = keys;
+  sk.hashed = hashed;
+  tile_bin_kernel<OP, F, WPB, POL><<<grid_for(n, kTile, kTileMinBlocks), kTileThreads, 0, s>>>(g, pl, words, keys, n,
+                                                                                             hashed, w, sk, occ);
   int st = status();
   if (st) return st;
   const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
-  const unsigned gt = (unsigned)(tiles < 0x7FFFFFFFull ? tiles : 0x7FFFFFFFull);
+  const unsigned gt = grid_for(tiles, 1, kTileMinBlocks);
   tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
   if ((st = status())) return st;
   tile_probe2_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
@@ -480,7 +500,7 @@ struct QueryOp {
   static int run(const QueryArgs& a) {
     if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.on) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, nullptr};
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
         return run_tiled<OP_QUERY, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
                                                 a.n, a.hashed, sk, nullptr, a.out, a.s);
       }
@@ -527,7 +547,7 @@ struct InsertOp {
         if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
         if (a.ev && cudaMemsetAsync(a.ev, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
         if (a.lost && cudaMemsetAsync(a.lost, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
-        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, a.ev, a.lost};
+        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, nullptr, false};
         st = run_tiled<OP_INSERT, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk, a.occ,
                                                nullptr, a.s);
         if (st) return st;
@@ -574,7 +594,7 @@ struct DeleteOp {
     }
     if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.on) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, nullptr};
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
         return run_tiled<OP_DELETE, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
                                                  a.occ, a.out, a.s);
       }
@@ -675,7 +695,8 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
 static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, void* ws, uint64_t ws_bytes) {
   TiledArgs t{};
   if (!ws || !tiled_applies(p, n, flags)) return t;
-  t.pl = make_plan(p, n, flags);
+  bool ok;
+  t.pl = make_plan(p, n, flags, ok);
   t.L = layout_for(t.pl, n, op);
   t.ws = ws;
   t.on = ws_bytes >= t.L.total && ((uintptr_t)ws % 256) == 0;
@@ -684,7 +705,8 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
 
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
   if (!params_ok(p) || !tiled_applies(p, n, flags)) return 0;
-  return layout_for(make_plan(p, n, flags), n, op).total;
+  bool ok;
+  return layout_for(make_plan(p, n, flags, ok), n, op).total;
 }
 
 int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* ok, int64_t* evictions,
