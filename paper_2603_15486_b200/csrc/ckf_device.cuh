@@ -42,6 +42,62 @@ __device__ __forceinline__ void ld_bucket_ro(const uint64_t* p, uint64_t (&w)[WP
   }
 }
 
+// L2 evict-last variants for the tiled path: the bucket region being probed
+// must outlive the record streams flowing past it in L2.
+__device__ __forceinline__ uint64_t evict_last_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ uint64_t evict_first_policy() {
+  uint64_t p;
+  asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+
+template <int WPB>
+__device__ __forceinline__ void ld_bucket_ro_el(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
+  if constexpr (WPB >= 4) {
+#pragma unroll
+    for (int s = 0; s < WPB / 4; ++s)
+      asm volatile("ld.global.nc.L1::no_allocate.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
+                   : "l"(p + 4 * s));
+  } else if constexpr (WPB == 2) {
+    asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                 : "=l"(w[0]), "=l"(w[1]) : "l"(p), "l"(evict_last_policy()));
+  } else {
+    ld_bucket_ro<WPB>(p, w);
+  }
+}
+
+template <int WPB>
+__device__ __forceinline__ void ld_bucket_rw_el(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
+  if constexpr (WPB >= 4) {
+#pragma unroll
+    for (int s = 0; s < WPB / 4; ++s)
+      asm volatile("ld.relaxed.gpu.global.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
+                   : "l"(p + 4 * s)
+                   : "memory");
+  } else if constexpr (WPB == 2) {
+    asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                 : "=l"(w[0]), "=l"(w[1]) : "l"(p), "l"(evict_last_policy()) : "memory");
+  } else {
+    ld_bucket_rw<WPB>(p, w);
+  }
+}
+
+// streaming record accesses: first out of L2
+__device__ __forceinline__ uint64_t ld_stream_ef(const uint64_t* a, uint64_t pol) {
+  uint64_t v;
+  asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.u64 %0, [%1], %2;" : "=l"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void st_stream_ef(uint64_t* a, uint64_t v, uint64_t pol) {
+  asm volatile("st.global.L2::cache_hint.u64 [%0], %1, %2;" ::"l"(a), "l"(v), "l"(pol) : "memory");
+}
+
 // Coherent bucket snapshot for the mutating kernels: relaxed gpu-scope loads
 // are served by L2 (where the CAS commits), never a stale L1 line.
 template <int WPB>

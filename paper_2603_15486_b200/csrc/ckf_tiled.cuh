@@ -92,8 +92,8 @@ __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t i) { atomicOr(b
 template <int OP, int F, int WPB, int POL>
 struct Logic {
   static __device__ __forceinline__ void fetch(const uint64_t* words, uint64_t bucket, uint64_t (&w)[WPB]) {
-    if constexpr (OP == OP_QUERY) ld_bucket_ro<WPB>(words + bucket * WPB, w);
-    else ld_bucket_rw<WPB>(words + bucket * WPB, w);
+    if constexpr (OP == OP_QUERY) ld_bucket_ro_el<WPB>(words + bucket * WPB, w);
+    else ld_bucket_rw_el<WPB>(words + bucket * WPB, w);
   }
   // tag: fp for the primary bucket, fp|choice for the alternate
   static __device__ __forceinline__ bool act(uint64_t* words, uint64_t bucket, uint64_t fp, uint64_t tag,
@@ -220,6 +220,7 @@ __device__ __forceinline__ void block_append(const uint64_t (&rec)[I], const uin
                                              const Plan& pl, uint64_t* __restrict__ out, uint32_t* gcnt,
                                              SplitSmem& sm, Overflow&& ovf) {
   const int tid = threadIdx.x;
+  const uint64_t pol = evict_first_policy();
   for (uint32_t r = tid; r < pl.R; r += kTileThreads) sm.hist[r] = 0;
   __syncthreads();
   uint32_t rank[I];
@@ -243,7 +244,7 @@ __device__ __forceinline__ void block_append(const uint64_t (&rec)[I], const uin
   for (uint32_t p = tid; p < total; p += kTileThreads) {
     const uint32_t r = sm.bin[p];
     const uint64_t off = (uint64_t)sm.gbase[r] + (p - sm.start[r]);
-    if (off < pl.cap) out[r * pl.cap + off] = sm.rec[p];
+    if (off < pl.cap) st_stream_ef(out + r * pl.cap + off, sm.rec[p], pol);
     else ovf(sm.rec[p], r);
   }
   __syncthreads();
@@ -298,6 +299,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_probe1_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
   __shared__ SplitSmem sm;
   using Lg = Logic<OP, F, WPB, POL>;
+  const uint64_t pol = evict_first_policy();
   uint32_t n_ok = 0, n_alt = 0;
   const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
   for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
@@ -321,7 +323,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       for (int q = 0; q < kProbeItems; ++q) {
         const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
         v[q] = off < cnt;
-        const uint64_t rc = v[q] ? src[off] : 0;
+        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
         unpack_rec(rc, r, pl, idx[q], i1[q], fp[q]);
         if (v[q]) Lg::fetch(words, i1[q], wv[q]);
       }
@@ -363,6 +365,7 @@ template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_probe2_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
   using Lg = Logic<OP, F, WPB, POL>;
+  const uint64_t pol = evict_first_policy();
   uint32_t n_ok = 0;
   const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
   for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
@@ -383,7 +386,7 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       for (int q = 0; q < kProbeItems; ++q) {
         const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
         v[q] = off < cnt;
-        const uint64_t rc = v[q] ? src[off] : 0;
+        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
         unpack_rec(rc, r, pl, idx[q], i2[q], fp[q]);
         if (v[q]) Lg::fetch(words, i2[q], wv[q]);
       }

@@ -52,7 +52,7 @@ def show(tag, best, ok, fpr):
 
 show("direct", *run(False))
 regions = [int(x) for x in os.environ.get("REGIONS", "1024,2048").split(",")]
-groups = [int(x) for x in os.environ.get("GROUPS", "4,8,32").split(",")]
+groups = [int(x) for x in os.environ.get("BINGROUPS", "4,8,32").split(",")]
 for reg, grp in itertools.product(regions, groups):
     os.environ["CKF_REGION_KB"] = str(reg)
     os.environ["CKF_BIN_GROUP"] = str(grp)
