@@ -71,23 +71,6 @@ __device__ __forceinline__ void ld_bucket_ro_el(const uint64_t* p, uint64_t (&w)
   }
 }
 
-template <int WPB>
-__device__ __forceinline__ void ld_bucket_rw_el(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
-  if constexpr (WPB >= 4) {
-#pragma unroll
-    for (int s = 0; s < WPB / 4; ++s)
-      asm volatile("ld.relaxed.gpu.global.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
-                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
-                   : "l"(p + 4 * s)
-                   : "memory");
-  } else if constexpr (WPB == 2) {
-    asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
-                 : "=l"(w[0]), "=l"(w[1]) : "l"(p), "l"(evict_last_policy()) : "memory");
-  } else {
-    ld_bucket_rw<WPB>(p, w);
-  }
-}
-
 // streaming record accesses: first out of L2
 __device__ __forceinline__ uint64_t ld_stream_ef(const uint64_t* a, uint64_t pol) {
   uint64_t v;
@@ -113,6 +96,23 @@ __device__ __forceinline__ void ld_bucket_rw(const uint64_t* p, uint64_t (&w)[WP
                    : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
                    : "l"(p + 4 * s)
                    : "memory");
+  }
+}
+
+template <int WPB>
+__device__ __forceinline__ void ld_bucket_rw_el(const uint64_t* p, uint64_t (&w)[WPB > 0 ? WPB : 1]) {
+  if constexpr (WPB >= 4) {
+#pragma unroll
+    for (int s = 0; s < WPB / 4; ++s)
+      asm volatile("ld.relaxed.gpu.global.L2::evict_last.v4.u64 {%0,%1,%2,%3}, [%4];"
+                   : "=l"(w[4 * s]), "=l"(w[4 * s + 1]), "=l"(w[4 * s + 2]), "=l"(w[4 * s + 3])
+                   : "l"(p + 4 * s)
+                   : "memory");
+  } else if constexpr (WPB == 2) {
+    asm volatile("ld.relaxed.gpu.global.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                 : "=l"(w[0]), "=l"(w[1]) : "l"(p), "l"(evict_last_policy()) : "memory");
+  } else {
+    ld_bucket_rw<WPB>(p, w);
   }
 }
 
@@ -404,6 +404,155 @@ __device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_
     cur_tag = make_tag(cfp, nc, g);
   }
   return {0u, g.max_evictions, tag_fp(cur_tag, g)};
+}
+
+// Same chain, compile-time bucket shape: every bucket the chain inspects is
+// fetched as one 256-bit snapshot (not word by word), the BFS candidates'
+// alternate buckets are fetched kEvictFetch at a time, and the CAS updates
+// start from those snapshots.  Decisions are taken in exactly the reference
+// order (first candidate with room, K:407-414), so the sequential parity mode
+// stays bit-identical.
+constexpr int kEvictFetch = 4;
+
+template <int F>
+__device__ __forceinline__ bool lane_cas_from(uint64_t* p, int lane, uint64_t expect, uint64_t repl, uint64_t w) {
+  using L = Lanes<F>;
+  while (true) {
+    if (L::get(w, lane) != expect) return false;
+    const uint64_t old = cas64(p, w, L::put(w, lane, repl));
+    if (old == w) return true;
+    w = old;
+  }
+}
+
+template <int F, int WPB, int POL>
+__device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2, const Geo& g) {
+  using L = Lanes<F>;
+  constexpr int kTpw = L::kTpw;
+  constexpr uint32_t kB = WPB * kTpw;
+  constexpr int kLim = kB / 2 ? kB / 2 : 1;
+  const uint64_t tag2 = make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g);
+  uint64_t st = rng_init(g.seed, h, g.worker) + kGolden;
+  uint64_t cur_b = i1, cur_tag = fp;
+  if (smix(st) & 1u) {
+    cur_b = i2;
+    cur_tag = tag2;
+  }
+  if (g.eviction == CKF_EVICT_DFS) {  // K:374-389
+    for (uint32_t n = 1; n <= g.max_evictions; ++n) {
+      st += kGolden;
+      const uint32_t victim = (uint32_t)(smix(st) % kB);
+      const uint64_t ev = swap_slot<F>(words, cur_b, victim, cur_tag, g);
+      if (ev == 0) return {1u, n, 0};
+      uint64_t nc;
+      const uint64_t efp = tag_fp(ev, g);
+      cur_b = alt_index<POL>(cur_b, efp, tag_choice(ev, g), g, nc);
+      cur_tag = make_tag(efp, nc, g);
+      if (try_insert_t<F, WPB>(words, cur_b, cur_tag) >= 0) return {1u, n, 0};
+    }
+    return {0u, g.max_evictions, tag_fp(cur_tag, g)};
+  }
+  // BFS (K:391-436)
+  for (uint32_t n = 1; n <= g.max_evictions; ++n) {
+    st += kGolden;
+    const uint32_t start = (uint32_t)(smix(st) % kB);
+    uint64_t* base = words + cur_b * WPB;
+    uint64_t cw[WPB];
+    ld_bucket_rw<WPB>(base, cw);
+    // collect_candidates (K:257-272) from the snapshot
+    uint32_t cslot[kLim];
+    uint64_t ctag[kLim];
+    int cnt = 0;
+#pragma unroll
+    for (uint32_t j = 0; j < kB; ++j) {
+      uint32_t s = start + j;
+      if (s >= kB) s -= kB;
+      uint64_t word = cw[0];
+#pragma unroll
+      for (int q = 1; q < WPB; ++q)
+        if ((int)(s / kTpw) == q) word = cw[q];
+      const uint64_t t = L::get(word, s % kTpw);
+      if (t && cnt < kLim) {
+#pragma unroll
+        for (int q = 0; q < kLim; ++q)
+          if (q == cnt) {
+            cslot[q] = s;
+            ctag[q] = t;
+          }
+        ++cnt;
+      }
+    }
+    if (cnt == 0) {  // drained by concurrent deletes: take a direct slot
+      if (try_insert_snap<F, WPB>(words, cur_b, cur_tag, cw) >= 0) return {1u, n, 0};
+      continue;
+    }
+    int chosen = -1;
+    uint64_t alt_b = 0, alt_tag = 0, aw_chosen[WPB];
+    for (int c0 = 0; c0 < cnt && chosen < 0; c0 += kEvictFetch) {
+      uint64_t aw[kEvictFetch][WPB], ab[kEvictFetch], at[kEvictFetch];
+#pragma unroll
+      for (int q = 0; q < kEvictFetch; ++q) {
+        if (c0 + q >= cnt) continue;
+        uint64_t ct = 0;
+#pragma unroll
+        for (int r = 0; r < kLim; ++r)
+          if (r == c0 + q) ct = ctag[r];
+        uint64_t tc;
+        const uint64_t cfp = tag_fp(ct, g);
+        ab[q] = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, tc);
+        at[q] = make_tag(cfp, tc, g);
+        ld_bucket_rw<WPB>(words + ab[q] * WPB, aw[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kEvictFetch; ++q) {
+        if (chosen >= 0 || c0 + q >= cnt) continue;
+        uint64_t any = 0;
+#pragma unroll
+        for (int j = 0; j < WPB; ++j) any |= L::zeros(aw[q][j]);
+        if (any) {
+          chosen = c0 + q;
+          alt_b = ab[q];
+          alt_tag = at[q];
+#pragma unroll
+          for (int j = 0; j < WPB; ++j) aw_chosen[j] = aw[q][j];
+        }
+      }
+    }
+    uint32_t os = 0;
+    uint64_t otag = 0;
+#pragma unroll
+    for (int r = 0; r < kLim; ++r)
+      if (r == (chosen >= 0 ? chosen : cnt - 1)) {
+        os = cslot[r];
+        otag = ctag[r];
+      }
+    uint64_t ow = cw[0];
+#pragma unroll
+    for (int q = 1; q < WPB; ++q)
+      if ((int)(os / kTpw) == q) ow = cw[q];
+    if (chosen >= 0) {
+      // two-step relocation: copy the candidate out, then swap ourselves in
+      const int aslot = try_insert_snap<F, WPB>(words, alt_b, alt_tag, aw_chosen);
+      if (aslot < 0) continue;  // the free lane raced away
+      if (lane_cas_from<F>(base + os / kTpw, os % kTpw, otag, cur_tag, ow)) return {1u, n, 0};
+      lane_cas<F>(words + alt_b * WPB + aslot / kTpw, aslot % kTpw, alt_tag, 0);  // rollback
+      continue;
+    }
+    // nobody has room: evict the last candidate and deepen (K:427-434)
+    if (!lane_cas_from<F>(base + os / kTpw, os % kTpw, otag, cur_tag, ow)) continue;
+    uint64_t nc;
+    const uint64_t cfp = tag_fp(otag, g);
+    cur_b = alt_index<POL>(cur_b, cfp, tag_choice(otag, g), g, nc);
+    cur_tag = make_tag(cfp, nc, g);
+  }
+  return {0u, g.max_evictions, tag_fp(cur_tag, g)};
+}
+
+template <int F, int WPB, int POL>
+__device__ __forceinline__ Outcome evict_any(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2,
+                                             const Geo& g) {
+  if constexpr (WPB > 0) return evict_chain_t<F, WPB, POL>(words, h, fp, i1, i2, g);
+  else return evict_chain<F, POL>(words, h, fp, i1, i2, g);
 }
 
 // ---------------------------------------------------------------------------

@@ -180,7 +180,7 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
         if (pos < cap) {
           rec[pos] = ckf_record{i, h, 0u, 0u};
         } else {  // queue overflow: evict in place, outcome only in dense outputs
-          Outcome o = evict_chain<F, POL>(words, h, fp, i1, i2, g);
+          Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
           n_ok += o.ok;
           ok[i] = (uint8_t)o.ok;
           if (ev) ev[i] = o.rounds;
@@ -193,7 +193,7 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
 }
 
 // Eviction pass over the queued keys (the ~4% whose pair was full at 95% load).
-template <int F, int POL>
+template <int F, int WPB, int POL>
 __global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
                                                        int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
                                                        ckf_record* __restrict__ rec, uint64_t cap,
@@ -206,7 +206,7 @@ __global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restri
     const uint64_t h = rec[r].lost;  // the direct pass parks the key hash here
     uint64_t fp, i1, i2;
     place<POL>(h, g, fp, i1, i2);
-    Outcome o = evict_chain<F, POL>(words, h, fp, i1, i2, g);
+    Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
     rec[r] = ckf_record{i, o.lost, o.rounds, o.ok};
     n_ok += o.ok;
     ok[i] = (uint8_t)o.ok;
@@ -240,7 +240,7 @@ __global__ void __launch_bounds__(kBlock) delete_kernel(Geo g, uint64_t* __restr
 
 // Parity mode: the reference's sequential insert_batch (K:510-529), one
 // device thread, same key order, same PRNG stream; bit-identical table.
-template <int F, int POL>
+template <int F, int WPB, int POL>
 __global__ void seq_insert_kernel(Geo g, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* ok, int64_t* ev,
                                   uint64_t* lost, ckf_record* rec, uint64_t cap, ckf_counters* ctr, long long* occ,
                                   bool hashed) {
@@ -250,9 +250,9 @@ __global__ void seq_insert_kernel(Geo g, uint64_t* words, const uint64_t* keys, 
     uint64_t fp, i1, i2;
     place<POL>(h, g, fp, i1, i2);
     Outcome o{1u, 0u, 0};
-    if (try_insert_rt<F>(words, i1, fp, g) < 0 &&
-        try_insert_rt<F>(words, i2, make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g), g) < 0)
-      o = evict_chain<F, POL>(words, h, fp, i1, i2, g);
+    if (try_insert_any<F, WPB>(words, i1, fp, g) < 0 &&
+        try_insert_any<F, WPB>(words, i2, make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g), g) < 0)
+      o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
     ok[i] = (uint8_t)o.ok;
     if (ev) ev[i] = o.rounds;
     if (lost) lost[i] = o.lost;
@@ -534,7 +534,7 @@ template <int F, int WPB, int POL>
 struct InsertOp {
   static int run(const InsertArgs& a) {
     if (a.sequential) {
-      seq_insert_kernel<F, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr,
+      seq_insert_kernel<F, WPB, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr,
                                                    a.occ, a.hashed);
       return status();
     }
@@ -564,7 +564,7 @@ struct InsertOp {
       // the queue length is only known on the device: a fixed full-residency grid
       // strides over it (empty queues exit immediately)
       unsigned egrid = (unsigned)sm_count() * 4;
-      evict_kernel<F, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ);
+      evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ);
       st = status();
     }
     return st;
