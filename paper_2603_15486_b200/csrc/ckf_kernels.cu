@@ -459,13 +459,21 @@ static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, ui
   }
   sk.keys = keys;
   sk.hashed = hashed;
-  tile_bin_kernel<OP, F, WPB, POL><<<grid_for(n, kTile, kTileMinBlocks), kTileThreads, 0, s>>>(g, pl, words, keys, n,
-                                                                                             hashed, w, sk, occ);
+  static bool attr_set = false;  // per template instance: opt in to > 48 KB dynamic smem
+  if (!attr_set) {
+    cudaFuncSetAttribute(tile_bin_kernel<OP, F, WPB, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SplitSmem));
+    cudaFuncSetAttribute(tile_probe1_kernel<OP, F, WPB, POL>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         (int)sizeof(SplitSmem));
+    attr_set = true;
+  }
+  tile_bin_kernel<OP, F, WPB, POL><<<grid_for(n, kTile, kTileMinBlocks), kTileThreads, sizeof(SplitSmem), s>>>(
+      g, pl, words, keys, n, hashed, w, sk, occ);
   int st = status();
   if (st) return st;
   const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
   const unsigned gt = grid_for(tiles, 1, kTileMinBlocks);
-  tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
+  tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, sizeof(SplitSmem), s>>>(g, pl, words, w, sk, occ);
   if ((st = status())) return st;
   tile_probe2_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
   if ((st = status())) return st;

@@ -34,9 +34,16 @@ constexpr int kTileThreads = 256;
 constexpr int kTileItems = 8;
 constexpr int kTile = kTileThreads * kTileItems;  // records per tile
 constexpr int kTileMinBlocks = 4;                  // >= 4 resident CTAs per SM (<= 64 registers)
-constexpr int kMaxBins = 1024;
+constexpr int kMaxBins = 512;
 constexpr int kCntStride = 32;                     // bin counters 128 B apart (one line each)
-constexpr int kProbeItems = 2;                     // bucket fetches in flight per thread
+// bucket fetches in flight per thread: reads can batch 4; the CAS ops keep
+// fewer snapshots live so nothing spills (spills are L2 traffic that evicts
+// the very table region the tile is working on)
+template <int OP>
+struct ProbeItems {
+  static constexpr int value = OP == 0 ? 4 : 2;
+};
+constexpr int kBinsPerThread = kMaxBins / kTileThreads;  // bin counters owned by each thread
 
 // Binning plan for one (table, batch) pair, computed on the host.
 struct Plan {
@@ -164,14 +171,26 @@ __device__ __forceinline__ void enqueue_evict_one(const Sink& sk, uint32_t idx, 
   else if (sk.ok) sk.ok[idx] = 0;
 }
 
-// ---- block-cooperative multi-split append ----
+// ---- block-cooperative multi-split append, software-pipelined ----
+//
+// A tile's records are counting-sorted by bin in one of two shared-memory
+// slots and one global atomic per (block, bin) reserves a run right after the
+// previous block's run of that bin ("stage").  The runs are written out
+// ("scatter") only after the NEXT tile has been loaded and staged, so the
+// reservation atomics' round trip overlaps the next tile's memory traffic.
+// Runs go out as contiguous stores; partial sectors meet their neighbours in
+// L2.  Records past a bin's capacity go to `ovf(rec, bin)` instead.
 
-struct SplitSmem {
+struct SplitSlot {
   uint32_t hist[kMaxBins];
   uint32_t start[kMaxBins];
   uint32_t gbase[kMaxBins];
   uint64_t rec[kTile];
   uint16_t bin[kTile];
+};
+
+struct SplitSmem {
+  SplitSlot slot[2];
   uint32_t warp_sums[kTileThreads / 32];
 };
 
@@ -210,44 +229,59 @@ __device__ __forceinline__ void block_exclusive_scan(const uint32_t* in, uint32_
   __syncthreads();
 }
 
-// Appends the block's valid records to their bins: records are counting-sorted
-// by bin in shared memory, one global atomic per (block, bin) reserves a run
-// right after the previous block's run of that bin, and the runs go out as
-// contiguous stores (partial sectors meet their neighbours in L2).  Records
-// past a bin's capacity go to `ovf(rec, bin)` instead.
-template <int I, class Overflow>
-__device__ __forceinline__ void block_append(const uint64_t (&rec)[I], const uint32_t (&bin)[I], const bool (&v)[I],
-                                             const Plan& pl, uint64_t* __restrict__ out, uint32_t* gcnt,
-                                             SplitSmem& sm, Overflow&& ovf) {
+// Pending reservations of one staged tile: thread t owns bins t, t+256, ...
+struct Pending {
+  uint32_t base[kBinsPerThread];
+};
+
+template <int I>
+__device__ __forceinline__ void split_stage(const uint64_t (&rec)[I], const uint32_t (&bin)[I], const bool (&v)[I],
+                                            const Plan& pl, uint32_t* gcnt, SplitSmem& sm, int slot, Pending& pend) {
+  SplitSlot& S = sm.slot[slot];
   const int tid = threadIdx.x;
-  const uint64_t pol = evict_first_policy();
-  for (uint32_t r = tid; r < pl.R; r += kTileThreads) sm.hist[r] = 0;
+  __syncthreads();  // the scatter that last used this slot is complete
+  for (uint32_t r = tid; r < pl.R; r += kTileThreads) S.hist[r] = 0;
   __syncthreads();
   uint32_t rank[I];
 #pragma unroll
-  for (int j = 0; j < I; ++j) rank[j] = v[j] ? atomicAdd(&sm.hist[bin[j]], 1u) : 0u;
+  for (int j = 0; j < I; ++j) rank[j] = v[j] ? atomicAdd(&S.hist[bin[j]], 1u) : 0u;
   __syncthreads();
-  block_exclusive_scan(sm.hist, sm.start, pl.R, sm.warp_sums);
-  for (uint32_t r = tid; r < pl.R; r += kTileThreads) {
-    const uint32_t c = sm.hist[r];
-    sm.gbase[r] = c ? atomicAdd(gcnt + (size_t)r * kCntStride, c) : 0u;
+  block_exclusive_scan(S.hist, S.start, pl.R, sm.warp_sums);
+  // issue the reservations; their results are only consumed by split_scatter
+#pragma unroll
+  for (int k = 0; k < kBinsPerThread; ++k) {
+    const uint32_t r = tid + k * kTileThreads;
+    const uint32_t c = r < pl.R ? S.hist[r] : 0u;
+    pend.base[k] = c ? atomicAdd(gcnt + (size_t)r * kCntStride, c) : 0u;
   }
 #pragma unroll
   for (int j = 0; j < I; ++j) {
     if (!v[j]) continue;
-    const uint32_t p = sm.start[bin[j]] + rank[j];
-    sm.rec[p] = rec[j];
-    sm.bin[p] = (uint16_t)bin[j];
+    const uint32_t p = S.start[bin[j]] + rank[j];
+    S.rec[p] = rec[j];
+    S.bin[p] = (uint16_t)bin[j];
+  }
+}
+
+template <class Overflow>
+__device__ __forceinline__ void split_scatter(const Plan& pl, uint64_t* __restrict__ out, SplitSmem& sm, int slot,
+                                              const Pending& pend, Overflow&& ovf) {
+  SplitSlot& S = sm.slot[slot];
+  const int tid = threadIdx.x;
+  const uint64_t pol = evict_first_policy();
+#pragma unroll
+  for (int k = 0; k < kBinsPerThread; ++k) {
+    const uint32_t r = tid + k * kTileThreads;
+    if (r < pl.R) S.gbase[r] = pend.base[k];
   }
   __syncthreads();
-  const uint32_t total = sm.start[pl.R - 1] + sm.hist[pl.R - 1];
+  const uint32_t total = S.start[pl.R - 1] + S.hist[pl.R - 1];
   for (uint32_t p = tid; p < total; p += kTileThreads) {
-    const uint32_t r = sm.bin[p];
-    const uint64_t off = (uint64_t)sm.gbase[r] + (p - sm.start[r]);
-    if (off < pl.cap) st_stream_ef(out + r * pl.cap + off, sm.rec[p], pol);
-    else ovf(sm.rec[p], r);
+    const uint32_t r = S.bin[p];
+    const uint64_t off = (uint64_t)S.gbase[r] + (p - S.start[r]);
+    if (off < pl.cap) st_stream_ef(out + r * pl.cap + off, S.rec[p], pol);
+    else ovf(S.rec[p], r);
   }
-  __syncthreads();
 }
 
 // ---- pass A: hash + bin by primary-bucket region ----
@@ -256,9 +290,28 @@ template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_bin_kernel(Geo g, Plan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n, bool hashed,
                     Work w, Sink sk, long long* occ) {
-  __shared__ SplitSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
   using Lg = Logic<OP, F, WPB, POL>;
   uint32_t n_ok = 0;
+  // a full bin (adversarial keys): resolve that key in place, randomly
+  auto ovf = [&](uint64_t rc, uint32_t r) {
+    uint32_t ii;
+    uint64_t i1, fp;
+    unpack_rec(rc, r, pl, ii, i1, fp);
+    uint64_t c;
+    const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, c);
+    if (Lg::first(words, i1, fp, g) || Lg::second(words, i2, fp, g)) {
+      ++n_ok;
+      if (OP != OP_INSERT) set_bit(sk.bits, ii);
+    } else if (OP == OP_INSERT) {
+      const uint64_t k = keys[ii];
+      enqueue_evict_one(sk, ii, hashed ? k : xxh64(k, g.seed));
+    }
+  };
+  Pending pend[2];
+  int slot = 0;
+  bool have_prev = false;
   for (uint64_t t0 = blockIdx.x * (uint64_t)kTile; t0 < n; t0 += (uint64_t)gridDim.x * kTile) {
     uint64_t rec[kTileItems];
     uint32_t bin[kTileItems];
@@ -273,22 +326,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       bin[j] = bin_of(i1, pl);
       rec[j] = pack_rec((uint32_t)i, i1 - (uint64_t)bin[j] * pl.rb, fp, pl);
     }
-    // a full bin (adversarial keys): resolve that key in place, randomly
-    block_append(rec, bin, v, pl, w.bin1, w.cnt1, sm, [&](uint64_t rc, uint32_t r) {
-      uint32_t ii;
-      uint64_t i1, fp;
-      unpack_rec(rc, r, pl, ii, i1, fp);
-      uint64_t c;
-      const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, c);
-      if (Lg::first(words, i1, fp, g) || Lg::second(words, i2, fp, g)) {
-        ++n_ok;
-        if (OP != OP_INSERT) set_bit(sk.bits, ii);
-      } else if (OP == OP_INSERT) {
-        const uint64_t k = keys[ii];
-        enqueue_evict_one(sk, ii, hashed ? k : xxh64(k, g.seed));
-      }
-    });
+    split_stage(rec, bin, v, pl, w.cnt1, sm, slot, pend[slot]);
+    if (have_prev) split_scatter(pl, w.bin1, sm, slot ^ 1, pend[slot ^ 1], ovf);
+    have_prev = true;
+    slot ^= 1;
   }
+  if (have_prev) split_scatter(pl, w.bin1, sm, slot ^ 1, pend[slot ^ 1], ovf);
   block_count_add(n_ok, 0, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
@@ -297,45 +340,67 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
 template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_probe1_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
-  __shared__ SplitSmem sm;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
   using Lg = Logic<OP, F, WPB, POL>;
+  constexpr int kProbeItems = ProbeItems<OP>::value;
   const uint64_t pol = evict_first_policy();
   uint32_t n_ok = 0, n_alt = 0;
-  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
+  auto ovf = [&](uint64_t rc, uint32_t r2) {
+    uint32_t ii;
+    uint64_t i2, fp;
+    unpack_rec(rc, r2, pl, ii, i2, fp);
+    if (Lg::second(words, i2, fp, g)) {
+      ++n_ok;
+      if (OP != OP_INSERT) set_bit(sk.bits, ii);
+    } else if (OP == OP_INSERT) {
+      const uint64_t k = sk.keys[ii];
+      enqueue_evict_one(sk, ii, sk.hashed ? k : xxh64(k, g.seed));
+    }
+  };
+  Pending pend[2];
+  int slot = 0;
+  bool have_prev = false;
+  constexpr int kItems = kTileItems / 2;  // records per thread per tile
+  constexpr int kTileB = kTileThreads * kItems;
+  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin * 2;
   for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
     uint32_t r;
     uint64_t off0;
-    tile_coords(s, pl, r, off0);
+    tile_coords(s >> 1, pl, r, off0);
+    off0 += (s & 1) * kTileB;
     const uint32_t c = w.cnt1[(size_t)r * kCntStride];
     const uint64_t cnt = c < pl.cap ? c : pl.cap;
     if (off0 >= cnt) continue;  // block-uniform
     const uint64_t* src = w.bin1 + r * pl.cap;
-    uint64_t rec[kTileItems];
-    uint32_t bin[kTileItems];
-    bool need[kTileItems];
+    uint64_t rec[kItems];
+    uint32_t bin[kItems];
+    bool need[kItems];
 #pragma unroll
-    for (int j0 = 0; j0 < kTileItems; j0 += kProbeItems) {
+    for (int j = 0; j < kItems; ++j) {
+      const uint64_t off = off0 + j * kTileThreads + threadIdx.x;
+      rec[j] = off < cnt ? ld_stream_ef(src + off, pol) : ~0ull;
+    }
+#pragma unroll
+    for (int j0 = 0; j0 < kItems; j0 += kProbeItems) {
       uint64_t fp[kProbeItems], i1[kProbeItems];
       uint32_t idx[kProbeItems];
       uint64_t wv[kProbeItems][WPB];
-      bool v[kProbeItems];
 #pragma unroll
       for (int q = 0; q < kProbeItems; ++q) {
-        const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
-        v[q] = off < cnt;
-        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
-        unpack_rec(rc, r, pl, idx[q], i1[q], fp[q]);
-        if (v[q]) Lg::fetch(words, i1[q], wv[q]);
+        unpack_rec(rec[j0 + q], r, pl, idx[q], i1[q], fp[q]);
+        if (rec[j0 + q] != ~0ull) Lg::fetch(words, i1[q], wv[q]);
       }
 #pragma unroll
       for (int q = 0; q < kProbeItems; ++q) {
         const int j = j0 + q;
-        const bool done = v[q] && Lg::act(words, i1[q], fp[q], fp[q], wv[q]);
+        const bool v = rec[j] != ~0ull;
+        const bool done = v && Lg::act(words, i1[q], fp[q], fp[q], wv[q]);
         if (done) {
           ++n_ok;
           if (OP != OP_INSERT) set_bit(sk.bits, idx[q]);
         }
-        need[j] = v[q] && !done;
+        need[j] = v && !done;
         n_alt += need[j];
         uint64_t cc;
         const uint64_t i2 = alt_index<POL>(i1[q], fp[q], 0, g, cc);
@@ -343,19 +408,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
         rec[j] = pack_rec(idx[q], i2 - (uint64_t)bin[j] * pl.rb, fp[q], pl);
       }
     }
-    block_append(rec, bin, need, pl, w.bin2, w.cnt2, sm, [&](uint64_t rc, uint32_t r2) {
-      uint32_t ii;
-      uint64_t i2, fp;
-      unpack_rec(rc, r2, pl, ii, i2, fp);
-      if (Lg::second(words, i2, fp, g)) {
-        ++n_ok;
-        if (OP != OP_INSERT) set_bit(sk.bits, ii);
-      } else if (OP == OP_INSERT) {
-        const uint64_t k = sk.keys[ii];
-        enqueue_evict_one(sk, ii, sk.hashed ? k : xxh64(k, g.seed));
-      }
-    });
+    split_stage(rec, bin, need, pl, w.cnt2, sm, slot, pend[slot]);
+    if (have_prev) split_scatter(pl, w.bin2, sm, slot ^ 1, pend[slot ^ 1], ovf);
+    have_prev = true;
+    slot ^= 1;
   }
+  if (have_prev) split_scatter(pl, w.bin2, sm, slot ^ 1, pend[slot ^ 1], ovf);
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
@@ -365,6 +423,7 @@ template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_probe2_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
   using Lg = Logic<OP, F, WPB, POL>;
+  constexpr int kProbeItems = ProbeItems<OP>::value;
   const uint64_t pol = evict_first_policy();
   uint32_t n_ok = 0;
   const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
@@ -376,6 +435,12 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     const uint64_t cnt = c < pl.cap ? c : pl.cap;
     if (off0 >= cnt) continue;
     const uint64_t* src = w.bin2 + r * pl.cap;
+    uint64_t rec[kTileItems];
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      const uint64_t off = off0 + j * kTileThreads + threadIdx.x;
+      rec[j] = off < cnt ? ld_stream_ef(src + off, pol) : ~0ull;
+    }
 #pragma unroll
     for (int j0 = 0; j0 < kTileItems; j0 += kProbeItems) {
       uint64_t fp[kProbeItems], i2[kProbeItems];
@@ -384,10 +449,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
       bool v[kProbeItems];
 #pragma unroll
       for (int q = 0; q < kProbeItems; ++q) {
-        const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
-        v[q] = off < cnt;
-        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
-        unpack_rec(rc, r, pl, idx[q], i2[q], fp[q]);
+        v[q] = rec[j0 + q] != ~0ull;
+        unpack_rec(rec[j0 + q], r, pl, idx[q], i2[q], fp[q]);
         if (v[q]) Lg::fetch(words, i2[q], wv[q]);
       }
 #pragma unroll
