@@ -355,17 +355,17 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
 // L2-tiled execution: plan + workspace layout (host side; see ckf_tiled.cuh)
 // ---------------------------------------------------------------------------
 
-constexpr uint64_t kRegionBytes = 16ull << 20;  // table bytes per bin: L2-resident while probed
+constexpr uint64_t kRegionBytes = 2ull << 20;   // table bytes per bin
 constexpr uint64_t kTiledMinTable = 48ull << 20; // below this the table is L2-resident anyway
 
 struct Layout {
-  uint64_t cnt, novf, list, ovf_h, ovf_x, bits, total;
+  uint64_t cnt1, cnt2, bin1, bin2, bits, total;
 };
 
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
-// Developer knobs for sweeps (tools/sweep_tiled.py): CKF_REGION_KB, and
-// CKF_TILED_AUTO=0 to disable the automatic choice of the tiled path.
+// Developer knobs for sweeps (tools/sweep_tiled.py): CKF_REGION_KB, CKF_BIN_GROUP,
+// CKF_TILED_AUTO (0 disables the automatic choice of the tiled path).
 static uint64_t env_u64(const char* name, uint64_t dflt) {
   const char* v = getenv(name);
   return v && *v ? strtoull(v, nullptr, 10) : dflt;
@@ -380,26 +380,30 @@ static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags, bool& ok)
   const uint64_t table = m * bucket_bytes;
   const bool forced = (flags & CKF_FORCE_TILED) != 0;
   const uint64_t region_pref = env_u64("CKF_REGION_KB", kRegionBytes >> 10) << 10;
-  // small forced tables still get ~16 bins so the multi-bin logic is exercised
-  const uint64_t region = forced && table < 16 * region_pref ? (table / 16 ? table / 16 : 1) : region_pref;
+  // small forced tables still get ~64 bins so the multi-bin logic is exercised
+  const uint64_t region = forced && table < 64 * region_pref ? (table / 64 ? table / 64 : 1) : region_pref;
   uint64_t rb = region / bucket_bytes;
   if (rb < 2) rb = 2;
+  const uint64_t max_rb = 1ull << (32 - p->payload_bits);  // bucket offset bits in a record
+  if (rb > max_rb) rb = max_rb;
   uint64_t R = (m + rb - 1) / rb;
-  if (R > (uint64_t)kMaxBins) R = kMaxBins;
+  if (R > (uint64_t)kMaxBins) {
+    R = kMaxBins;
+    rb = (m + R - 1) / R;
+    if (rb > max_rb) return pl;
+  }
   rb = (m + R - 1) / R;  // balance the regions
   R = (m + rb - 1) / rb;
   if (rb < 2) return pl;
-  uint32_t lb = 0;
-  while ((1ull << lb) < rb) ++lb;
-  const uint32_t idx_bits = 64 - lb - p->payload_bits;
-  if (idx_bits < 64 && (n >> (idx_bits > 63 ? 63 : idx_bits)) != 0) return pl;  // index must fit a record
   pl.rb = (uint32_t)rb;
   pl.R = (uint32_t)R;
   pl.pb = p->payload_bits;
-  pl.lb = lb;
   pl.div_magic = ~0ull / rb + 1;  // Lemire fastdiv: exact bucket / rb for bucket < 2^32
+  pl.group = (uint32_t)env_u64("CKF_BIN_GROUP", 8);
+  if (pl.group < 1) pl.group = 1;
   const double per = (double)n / (double)R;
-  pl.cap = ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + kProbeRecs - 1) / kProbeRecs * kProbeRecs;
+  pl.cap = (uint64_t)(per + 4.0 * std::sqrt(per) + 64.0);
+  pl.tiles_per_bin = (uint32_t)((pl.cap + kTile - 1) / kTile);
   ok = true;
   return pl;
 }
@@ -408,7 +412,8 @@ static bool tiled_applies(const ckf_params* p, uint64_t n, unsigned flags) {
   if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
   const uint32_t wpb = p->words_per_bucket;
   if (wpb != 2 && wpb != 4 && wpb != 8) return false;
-  if (p->bucket_count > 0xFFFFFFFFull || p->bucket_count < 16 || n >= 0xFFFFFFFFull || n == 0) return false;
+  if (p->bucket_count > 0xFFFFFFFFull || p->bucket_count < 64 || n >= 0xFFFFFFFFull || n == 0) return false;
+  if (p->payload_bits > 24) return false;  // record = idx:32 | offset | fp
   if (!(flags & CKF_FORCE_TILED)) {
     if (!env_u64("CKF_TILED_AUTO", 1)) return false;
     const uint64_t table = p->bucket_count * wpb * 8ull;
@@ -421,48 +426,48 @@ static bool tiled_applies(const ckf_params* p, uint64_t n, unsigned flags) {
 }
 
 static Layout layout_for(const Plan& pl, uint64_t n, int op) {
-  (void)op;
   Layout L{};
-  L.cnt = 0;
-  L.novf = align256(2ull * kMaxBins * kCntStride * 4);
-  uint64_t off = L.novf + 256;  // two counters, 128 B apart
-  L.list = off;
-  off = align256(off + 2ull * pl.R * pl.cap * 8);
-  L.ovf_h = off;
-  off = align256(off + 2ull * n * 8);
-  L.ovf_x = off;
-  off = align256(off + 2ull * n * 4);
+  L.cnt1 = 0;
+  L.cnt2 = align256((uint64_t)pl.R * kCntStride * 4);
+  uint64_t off = 2 * L.cnt2;
+  const uint64_t recs = (uint64_t)pl.R * pl.cap;
+  L.bin1 = off;
+  off = align256(off + recs * 8);
+  L.bin2 = off;
+  off = align256(off + recs * 8);
   L.bits = off;
-  off = align256(off + (n + 31) / 32 * 4);
+  if (op != CKF_OP_INSERT) off = align256(off + (n + 31) / 32 * 4);
   L.total = off;
   return L;
 }
 
 static Work work_view(void* ws, const Layout& L) {
   char* b = (char*)ws;
-  return Work{(uint32_t*)(b + L.cnt),    (unsigned long long*)(b + L.novf), (uint64_t*)(b + L.list),
-              (uint64_t*)(b + L.ovf_h), (uint32_t*)(b + L.ovf_x),          (uint32_t*)(b + L.bits)};
+  return Work{(uint32_t*)(b + L.cnt1), (uint32_t*)(b + L.cnt2), (uint64_t*)(b + L.bin1), (uint64_t*)(b + L.bin2),
+              (uint32_t*)(b + L.bits)};
 }
 
-// Tiled run of one op: pass A (split) + pass B/C (probe) (+ bit expansion for
-// query/delete; insert's eviction pass follows in the caller).
+// Tiled run of one op: pass A/B/C (+ bit expansion for query/delete).
 template <int OP, int F, int WPB, int POL>
 static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, uint64_t* words, const uint64_t* keys,
                      uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out, cudaStream_t s) {
   Work w = work_view(ws, L);
-  if (cudaMemsetAsync(ws, 0, L.list, s) != cudaSuccess) return cuda_error();  // bin + overflow counters
-  if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
-  sk.bits = w.bits;
+  if (cudaMemsetAsync(ws, 0, L.bin1, s) != cudaSuccess) return cuda_error();  // bin counters
+  if (OP != OP_INSERT) {
+    if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
+    sk.bits = w.bits;
+  }
   sk.keys = keys;
   sk.hashed = hashed;
-  tile_split_kernel<POL><<<grid_for(n, kSplitTile, 5), kTileThreads, sizeof(SplitSmem), s>>>(g, pl, keys, n, hashed,
-                                                                                            w);
+  tile_bin_kernel<OP, F, WPB, POL><<<grid_for(n, kTile, kTileMinBlocks), kTileThreads, 0, s>>>(g, pl, words, keys, n,
+                                                                                             hashed, w, sk, occ);
   int st = status();
   if (st) return st;
-  const unsigned gp = grid_for((uint64_t)pl.R * pl.cap, (uint64_t)kTileThreads * kProbeRecs, 8);
-  tile_probe_kernel<OP, F, WPB, POL, false><<<gp, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ, n);
+  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
+  const unsigned gt = grid_for(tiles, 1, kTileMinBlocks);
+  tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
   if ((st = status())) return st;
-  tile_probe_kernel<OP, F, WPB, POL, true><<<gp, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ, n);
+  tile_probe2_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
   if ((st = status())) return st;
   if (OP != OP_INSERT) {
     expand_bits_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out);

@@ -1,31 +1,27 @@
-// ckf_tiled.cuh -- L2-tiled execution of large batches ("coarse dual-list").
+// ckf_tiled.cuh -- L2-tiled execution of large batches.
 //
 // Why: one insert / query / delete touches one or two random 32-byte buckets.
 // Measured on B200 (profiles/r01_probe_ceiling.txt), random 32 B sector reads
 // top out at ~48 G/s at 512 MiB (~1.5 TB/s useful, a quarter of the 6.4 TB/s
-// streaming peak) and a DRAM-resident CAS at ~24 G/s, while the same accesses
-// inside an L2-resident 16-64 MiB window run at 100-150 G/s even with a
-// concurrent multi-GB stream (profiles/r01_probe_atomics.txt,
-// r01_probe_l2mix.txt).  When a batch holds many keys per bucket (the
-// benchmark: 15 keys per bucket) the tiled path therefore
+// streaming peak): HBM3e is row-activation bound on random sectors, and a
+// DRAM-resident atomic costs ~2 such accesses (profiles/r01_probe_atomics.txt:
+// 24 G CAS/s at 512 MiB vs 120 G/s L2-resident).  When a batch holds many keys
+// per bucket (the benchmark inserts 15 keys per bucket) the same buckets are
+// fetched again and again.  The tiled path therefore
 //
-//   pass A  hashes every key once and appends a packed 8-byte record
-//           (batch index | bucket offset in region | fingerprint) to TWO
-//           lists: list A, binned by the L2-sized table region (R ≈ table /
-//           16 MiB) of its primary bucket, and list B, binned by the region of
-//           its alternate bucket.  Few bins -> each block writes long
-//           contiguous runs and takes one counter atomic per bin per tile;
-//   pass B  streams list A bin after bin with a flat grid: the region being
-//           worked on is L2-resident, so the bucket access is an L2 hit; a
-//           resolved key sets its bit in an L2-resident n-bit map;
-//   pass C  streams list B the same way; keys whose bit is already set are
-//           skipped, the rest try their alternate bucket.
-// Every DRAM stream is sequential; no block synchronisation in the probe
-// passes.  Semantics are unchanged: batch ops are concurrent and this is one
-// legal schedule of them (every key tries i1 before i2, as in K:359-362).
-// A record whose bin is full (adversarial keys) is parked as (hash, index) on
-// an overflow list of capacity n that the same probe pass drains after the
-// bins, so correctness never depends on the binning statistics.
+//   pass A  hashes the keys and bins them by the table region (R regions of
+//           `rb` buckets) of their primary bucket, as packed 8-byte records
+//           (batch index | bucket offset in region | fingerprint);
+//   pass B  walks the bins `group` at a time -- those regions are L2-resident
+//           -- and resolves every key whose primary bucket answers it; the rest
+//           are re-binned by the region of their alternate bucket;
+//   pass C  walks those bins the same way for the alternate bucket;
+// and the per-key results are merged through an L2-resident bitmap (n/8
+// bytes).  Every DRAM stream is sequential; the bucket accesses hit L2.
+// Semantics are unchanged: batch ops are concurrent and this is one legal
+// schedule of them (every key tries i1 before i2, as in K:359-362).  A full bin
+// (adversarial keys) resolves its key in place on the direct path, so
+// correctness never depends on the binning statistics.
 #pragma once
 
 #include "ckf_device.cuh"
@@ -36,50 +32,51 @@ enum { OP_QUERY = 0, OP_INSERT = 1, OP_DELETE = 2 };
 
 constexpr int kTileThreads = 256;
 constexpr int kTileItems = 8;
-constexpr int kTile = kTileThreads * kTileItems;  // keys per pass-A tile
-constexpr int kMaxBins = 128;                      // per list
+constexpr int kTile = kTileThreads * kTileItems;  // records per tile
+constexpr int kTileMinBlocks = 4;                  // >= 4 resident CTAs per SM (<= 64 registers)
+constexpr int kMaxBins = 1024;
 constexpr int kCntStride = 32;                     // bin counters 128 B apart (one line each)
-constexpr int kProbeRecs = 4;                      // records per thread per probe iteration
+constexpr int kProbeItems = 2;                     // bucket fetches in flight per thread
 
 // Binning plan for one (table, batch) pair, computed on the host.
 struct Plan {
-  uint64_t div_magic;  // region = mulhi(bucket, div_magic) == bucket / rb  (bucket < 2^32)
-  uint64_t cap;        // record slots per bin (multiple of kProbeRecs)
+  uint64_t div_magic;  // bin = mulhi(bucket, div_magic)  (== bucket / rb for bucket < 2^32)
+  uint64_t cap;        // record slots per bin
   uint32_t rb;         // buckets per region
-  uint32_t R;          // bins per list
-  uint32_t pb;         // fingerprint bits in a record
-  uint32_t lb;         // bucket-offset bits in a record
+  uint32_t R;          // number of bins
+  uint32_t pb;         // payload (fingerprint) bits in a record
+  uint32_t group;      // bins probed concurrently
+  uint32_t tiles_per_bin;
 };
 
 __device__ __forceinline__ uint32_t bin_of(uint64_t bucket, const Plan& pl) {
   return (uint32_t)__umul64hi(bucket, pl.div_magic);
 }
 
-// record = index << (lb+pb) | (bucket - bin*rb) << pb | fp
-__device__ __forceinline__ uint64_t pack_rec(uint64_t idx, uint64_t bucket, uint32_t bin, uint64_t fp,
-                                             const Plan& pl) {
-  return (idx << (pl.lb + pl.pb)) | ((bucket - (uint64_t)bin * pl.rb) << pl.pb) | fp;
+// record = index << 32 | (bucket - bin*rb) << pb | fp
+__device__ __forceinline__ uint64_t pack_rec(uint32_t idx, uint64_t local, uint64_t fp, const Plan& pl) {
+  return ((uint64_t)idx << 32) | (local << pl.pb) | fp;
 }
-__device__ __forceinline__ void unpack_rec(uint64_t rec, uint32_t bin, const Plan& pl, uint32_t& idx,
-                                           uint64_t& bucket, uint64_t& fp) {
-  idx = (uint32_t)(rec >> (pl.lb + pl.pb));
-  fp = rec & ((1ull << pl.pb) - 1u);
-  bucket = (uint64_t)bin * pl.rb + ((rec >> pl.pb) & ((1ull << pl.lb) - 1u));
+__device__ __forceinline__ void unpack_rec(uint64_t rec, uint32_t bin, const Plan& pl, uint32_t& idx, uint64_t& bucket,
+                                           uint64_t& fp) {
+  idx = (uint32_t)(rec >> 32);
+  const uint32_t lo = (uint32_t)rec;
+  fp = lo & ((1u << pl.pb) - 1u);
+  bucket = (uint64_t)bin * pl.rb + (lo >> pl.pb);
 }
 
 // Workspace views (layout: layout_for in ckf_kernels.cu).
 struct Work {
-  uint32_t* cnt;    // [2][kMaxBins*kCntStride] records appended per bin (list A, list B; may exceed cap)
-  unsigned long long* novf;  // [2 lines] overflow-list lengths
-  uint64_t* list;   // [2][R*cap] records, list A then list B
-  uint64_t* ovf_h;  // [2][n] hashes of keys whose bin was full (adversarial input only)
-  uint32_t* ovf_x;  // [2][n] their batch indexes
-  uint32_t* bits;   // [ceil(n/32)] resolved / result bit per key
+  uint32_t* cnt1;   // [R*kCntStride] records appended per primary bin (may exceed cap)
+  uint32_t* cnt2;   // [R*kCntStride] per alternate bin
+  uint64_t* bin1;   // [R*cap] records binned by primary region
+  uint64_t* bin2;   // [R*cap] records binned by alternate region
+  uint32_t* bits;   // [ceil(n/32)] result bitmap (query / delete)
 };
 
 // What happens to a resolved / unresolved key.
 struct Sink {
-  uint32_t* bits;         // resolved bit per key (query/delete: the result)
+  uint32_t* bits;         // query/delete: result bit per key
   ckf_record* rec;        // insert: eviction queue
   uint64_t rec_cap;
   ckf_counters* ctr;
@@ -95,8 +92,8 @@ __device__ __forceinline__ void set_bit(uint32_t* bits, uint32_t i) { atomicOr(b
 template <int OP, int F, int WPB, int POL>
 struct Logic {
   static __device__ __forceinline__ void fetch(const uint64_t* words, uint64_t bucket, uint64_t (&w)[WPB]) {
-    if constexpr (OP == OP_QUERY) ld_bucket_ro<WPB>(words + bucket * WPB, w);
-    else ld_bucket_rw<WPB>(words + bucket * WPB, w);
+    if constexpr (OP == OP_QUERY) ld_bucket_ro_el<WPB>(words + bucket * WPB, w);
+    else ld_bucket_rw_el<WPB>(words + bucket * WPB, w);
   }
   // tag: fp for the primary bucket, fp|choice for the alternate
   static __device__ __forceinline__ bool act(uint64_t* words, uint64_t bucket, uint64_t fp, uint64_t tag,
@@ -130,10 +127,15 @@ struct Logic {
   }
 };
 
-__device__ __forceinline__ void enqueue_evict_one(const Sink& sk, uint32_t idx, uint64_t h) {
-  const uint64_t pos = atomicAdd(&sk.ctr->n_queued, 1ull);
-  if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, h, 0u, 0u};
-  else if (sk.ok) sk.ok[idx] = 0;  // queue overflow: reported as not stored
+// Probe-pass tile order: the tiles of `group` consecutive bins are
+// interleaved, so the CTAs in flight spread over `group` table regions (kept
+// L2-resident) instead of piling onto one region's buckets (CAS contention).
+__device__ __forceinline__ void tile_coords(uint64_t s, const Plan& pl, uint32_t& bin, uint64_t& off0) {
+  const uint32_t grp = pl.R < pl.group ? pl.R : pl.group;
+  const uint64_t per_group = (uint64_t)grp * pl.tiles_per_bin;
+  const uint64_t gidx = s / per_group, q = s % per_group;
+  bin = (uint32_t)(gidx * grp + q % grp);
+  off0 = (q / grp) * kTile;
 }
 
 // Unresolved insert after both buckets: hand (index, hash) to the eviction
@@ -151,222 +153,255 @@ __device__ __forceinline__ void enqueue_evict(const Sink& sk, bool need, uint32_
   const uint64_t pos = base + __popc(qm & ((1u << lane) - 1u));
   const uint64_t k = sk.keys[idx];
   if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, sk.hashed ? k : xxh64(k, g.seed), 0u, 0u};
+  // queue overflow cannot happen through the facade (capacity = n); the key
+  // is then reported as not stored
   else if (sk.ok) sk.ok[idx] = 0;
 }
 
-// ---- pass A: hash once, append to list A (primary region) and list B ----
-
-constexpr int kSplitItems = 4;                          // keys per thread per split tile
-constexpr int kSplitTile = kTileThreads * kSplitItems;  // keys per tile (2 records each)
-constexpr int kWarps = kTileThreads / 32;
-
-struct SplitSmem {
-  uint32_t whist[kWarps][2 * kMaxBins];  // per-warp record count per virtual bin, then warp base
-  uint32_t start[2 * kMaxBins];          // tile-level start of each virtual bin
-  uint32_t gbase[2 * kMaxBins];          // reserved global offset of the tile's run
-  uint32_t warp_sums[kWarps];
-  uint64_t rec[2 * kSplitTile];
-  uint8_t vbin[2 * kSplitTile];          // virtual bin = list * R + bin
-};
-
-// Warp-level multi-split rank: lanes with the same virtual bin are grouped
-// with __match_any_sync; the group's first lane bumps the warp's private
-// counter.  No shared-memory atomics (few bins would serialise them).
-__device__ __forceinline__ uint32_t warp_rank(uint32_t vb, bool valid, uint32_t* whist_w) {
-  const unsigned full = 0xffffffffu;
-  const int lane = threadIdx.x & 31;
-  const unsigned same = __match_any_sync(full, valid ? vb : 0x10000u + lane);
-  const int leader = __ffs(same) - 1;
-  uint32_t base = 0;
-  if (valid && lane == leader) {
-    base = whist_w[vb];
-    whist_w[vb] = base + __popc(same);
-  }
-  base = __shfl_sync(full, base, leader);
-  return base + __popc(same & ((1u << lane) - 1u));
+__device__ __forceinline__ void enqueue_evict_one(const Sink& sk, uint32_t idx, uint64_t h) {
+  const uint64_t pos = atomicAdd(&sk.ctr->n_queued, 1ull);
+  if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, h, 0u, 0u};
+  else if (sk.ok) sk.ok[idx] = 0;
 }
 
-template <int POL>
-__global__ void __launch_bounds__(kTileThreads)
-    tile_split_kernel(Geo g, Plan pl, const uint64_t* __restrict__ keys, uint64_t n, bool hashed, Work w) {
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  SplitSmem& sm = *reinterpret_cast<SplitSmem*>(smem_raw);
-  const uint64_t pol = evict_first_policy();
-  const uint32_t V = 2 * pl.R;  // virtual bins (<= kTileThreads)
-  const int tid = threadIdx.x, wid = tid >> 5;
-  for (uint64_t t0 = blockIdx.x * (uint64_t)kSplitTile; t0 < n; t0 += (uint64_t)gridDim.x * kSplitTile) {
-    for (uint32_t x = tid; x < kWarps * 2 * kMaxBins; x += kTileThreads) (&sm.whist[0][0])[x] = 0;
-    __syncthreads();
-    uint64_t rec[2 * kSplitItems];
-    uint32_t vb[2 * kSplitItems], rk[2 * kSplitItems];
-    bool v[kSplitItems];
+// ---- block-cooperative multi-split append ----
+
+struct SplitSmem {
+  uint32_t hist[kMaxBins];
+  uint32_t start[kMaxBins];
+  uint32_t gbase[kMaxBins];
+  uint64_t rec[kTile];
+  uint16_t bin[kTile];
+  uint32_t warp_sums[kTileThreads / 32];
+};
+
+// Exclusive prefix sum of in[0..R) into out[] by the whole block.
+__device__ __forceinline__ void block_exclusive_scan(const uint32_t* in, uint32_t* out, uint32_t R,
+                                                     uint32_t* warp_sums) {
+  constexpr int NW = kTileThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (R + kTileThreads - 1) / kTileThreads;
+  const uint32_t lo = min(tid * per, R), hi = min(lo + per, R);
+  uint32_t sum = 0;
+  for (uint32_t k = lo; k < hi; ++k) sum += in[k];
+  uint32_t x = sum;
 #pragma unroll
-    for (int j = 0; j < kSplitItems; ++j) {
-      const uint64_t i = t0 + j * kTileThreads + tid;
+  for (int d = 1; d < 32; d <<= 1) {
+    uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t v = lane < NW ? warp_sums[lane] : 0, s = v;
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1) {
+      uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= d) s += y;
+    }
+    if (lane < NW) warp_sums[lane] = s - v;
+  }
+  __syncthreads();
+  uint32_t run = warp_sums[wid] + x - sum;
+  for (uint32_t k = lo; k < hi; ++k) {
+    out[k] = run;
+    run += in[k];
+  }
+  __syncthreads();
+}
+
+// Appends the block's valid records to their bins: records are counting-sorted
+// by bin in shared memory, one global atomic per (block, bin) reserves a run
+// right after the previous block's run of that bin, and the runs go out as
+// contiguous stores (partial sectors meet their neighbours in L2).  Records
+// past a bin's capacity go to `ovf(rec, bin)` instead.
+template <int I, class Overflow>
+__device__ __forceinline__ void block_append(const uint64_t (&rec)[I], const uint32_t (&bin)[I], const bool (&v)[I],
+                                             const Plan& pl, uint64_t* __restrict__ out, uint32_t* gcnt,
+                                             SplitSmem& sm, Overflow&& ovf) {
+  const int tid = threadIdx.x;
+  const uint64_t pol = evict_first_policy();
+  for (uint32_t r = tid; r < pl.R; r += kTileThreads) sm.hist[r] = 0;
+  __syncthreads();
+  uint32_t rank[I];
+#pragma unroll
+  for (int j = 0; j < I; ++j) rank[j] = v[j] ? atomicAdd(&sm.hist[bin[j]], 1u) : 0u;
+  __syncthreads();
+  block_exclusive_scan(sm.hist, sm.start, pl.R, sm.warp_sums);
+  for (uint32_t r = tid; r < pl.R; r += kTileThreads) {
+    const uint32_t c = sm.hist[r];
+    sm.gbase[r] = c ? atomicAdd(gcnt + (size_t)r * kCntStride, c) : 0u;
+  }
+#pragma unroll
+  for (int j = 0; j < I; ++j) {
+    if (!v[j]) continue;
+    const uint32_t p = sm.start[bin[j]] + rank[j];
+    sm.rec[p] = rec[j];
+    sm.bin[p] = (uint16_t)bin[j];
+  }
+  __syncthreads();
+  const uint32_t total = sm.start[pl.R - 1] + sm.hist[pl.R - 1];
+  for (uint32_t p = tid; p < total; p += kTileThreads) {
+    const uint32_t r = sm.bin[p];
+    const uint64_t off = (uint64_t)sm.gbase[r] + (p - sm.start[r]);
+    if (off < pl.cap) st_stream_ef(out + r * pl.cap + off, sm.rec[p], pol);
+    else ovf(sm.rec[p], r);
+  }
+  __syncthreads();
+}
+
+// ---- pass A: hash + bin by primary-bucket region ----
+
+template <int OP, int F, int WPB, int POL>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tile_bin_kernel(Geo g, Plan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n, bool hashed,
+                    Work w, Sink sk, long long* occ) {
+  __shared__ SplitSmem sm;
+  using Lg = Logic<OP, F, WPB, POL>;
+  uint32_t n_ok = 0;
+  for (uint64_t t0 = blockIdx.x * (uint64_t)kTile; t0 < n; t0 += (uint64_t)gridDim.x * kTile) {
+    uint64_t rec[kTileItems];
+    uint32_t bin[kTileItems];
+    bool v[kTileItems];
+#pragma unroll
+    for (int j = 0; j < kTileItems; ++j) {
+      const uint64_t i = t0 + j * kTileThreads + threadIdx.x;
       v[j] = i < n;
       const uint64_t h = v[j] ? load_hash(keys, i, g.seed, hashed) : 0;
       uint64_t fp, i1, i2;
       place<POL>(h, g, fp, i1, i2);
-      const uint32_t ba = bin_of(i1, pl), bb = bin_of(i2, pl);
-      rec[2 * j] = pack_rec(i, i1, ba, fp, pl);
-      rec[2 * j + 1] = pack_rec(i, i2, bb, fp, pl);
-      vb[2 * j] = ba;
-      vb[2 * j + 1] = pl.R + bb;
+      bin[j] = bin_of(i1, pl);
+      rec[j] = pack_rec((uint32_t)i, i1 - (uint64_t)bin[j] * pl.rb, fp, pl);
     }
-#pragma unroll
-    for (int j = 0; j < 2 * kSplitItems; ++j) rk[j] = warp_rank(vb[j], v[j / 2], sm.whist[wid]);
-    __syncthreads();
-    // per virtual bin: column prefix over warps, tile total, block scan, reservation
-    uint32_t total = 0;
-    if ((uint32_t)tid < V) {
-#pragma unroll
-      for (int q = 0; q < kWarps; ++q) {
-        const uint32_t c = sm.whist[q][tid];
-        sm.whist[q][tid] = total;
-        total += c;
-      }
-    }
-    {  // exclusive block scan of `total` (one virtual bin per thread)
-      const int lane = tid & 31;
-      uint32_t x = total;
-#pragma unroll
-      for (int d = 1; d < 32; d <<= 1) {
-        const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
-        if (lane >= d) x += y;
-      }
-      if (lane == 31) sm.warp_sums[wid] = x;
-      __syncthreads();
-      uint32_t off = 0;
-#pragma unroll
-      for (int q = 0; q < kWarps; ++q) off += q < wid ? sm.warp_sums[q] : 0u;
-      if ((uint32_t)tid < V) {
-        sm.start[tid] = off + x - total;
-        const uint32_t list = (uint32_t)tid >= pl.R;
-        sm.gbase[tid] =
-            total ? atomicAdd(w.cnt + (size_t)list * kMaxBins * kCntStride + (size_t)(tid - list * pl.R) * kCntStride,
-                              total)
-                  : 0u;
-      }
-    }
-    __syncthreads();
-#pragma unroll
-    for (int j = 0; j < 2 * kSplitItems; ++j) {
-      if (!v[j / 2]) continue;
-      const uint32_t p = sm.start[vb[j]] + sm.whist[wid][vb[j]] + rk[j];
-      sm.rec[p] = rec[j];
-      sm.vbin[p] = (uint8_t)vb[j];
-    }
-    __syncthreads();
-    const uint32_t nrec = 2 * (uint32_t)min((uint64_t)kSplitTile, n - t0);
-    for (uint32_t p = tid; p < nrec; p += kTileThreads) {
-      const uint32_t vv = sm.vbin[p];
-      const uint32_t list = vv >= pl.R, r = vv - list * pl.R;
-      const uint64_t off = (uint64_t)sm.gbase[vv] + (p - sm.start[vv]);
-      if (off < pl.cap) {
-        st_stream_ef(w.list + (uint64_t)list * pl.R * pl.cap + (uint64_t)r * pl.cap + off, sm.rec[p], pol);
-      } else {
-        // a full bin (adversarial keys): park (hash, index) on the overflow
-        // list that the matching probe pass drains after its bins
-        const uint32_t ii = (uint32_t)(sm.rec[p] >> (pl.lb + pl.pb));
+    // a full bin (adversarial keys): resolve that key in place, randomly
+    block_append(rec, bin, v, pl, w.bin1, w.cnt1, sm, [&](uint64_t rc, uint32_t r) {
+      uint32_t ii;
+      uint64_t i1, fp;
+      unpack_rec(rc, r, pl, ii, i1, fp);
+      uint64_t c;
+      const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, c);
+      if (Lg::first(words, i1, fp, g) || Lg::second(words, i2, fp, g)) {
+        ++n_ok;
+        if (OP != OP_INSERT) set_bit(sk.bits, ii);
+      } else if (OP == OP_INSERT) {
         const uint64_t k = keys[ii];
-        const uint64_t pos = atomicAdd(w.novf + list * 16, 1ull);
-        w.ovf_h[(uint64_t)list * n + pos] = hashed ? k : xxh64(k, g.seed);
-        w.ovf_x[(uint64_t)list * n + pos] = ii;
+        enqueue_evict_one(sk, ii, hashed ? k : xxh64(k, g.seed));
       }
-    }
-    __syncthreads();
+    });
   }
+  block_count_add(n_ok, 0, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
-// ---- passes B and C: flat streams over list A (primary) / list B (alternate) ----
+// ---- pass B: primary buckets; misses re-binned by alternate region ----
 
-template <int OP, int F, int WPB, int POL, bool SECOND>
-__global__ void __launch_bounds__(kTileThreads)
-    tile_probe_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ, uint64_t n) {
+template <int OP, int F, int WPB, int POL>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tile_probe1_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
+  __shared__ SplitSmem sm;
   using Lg = Logic<OP, F, WPB, POL>;
   const uint64_t pol = evict_first_policy();
-  const uint64_t* list = w.list + (SECOND ? (uint64_t)pl.R * pl.cap : 0);
-  const uint32_t* cnt = w.cnt + (SECOND ? (size_t)kMaxBins * kCntStride : 0);
-  const uint64_t total = (uint64_t)pl.R * pl.cap;  // positions (multiple of kProbeRecs)
-  const uint64_t gtid = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x;
-  const uint64_t nthreads = (uint64_t)gridDim.x * blockDim.x;
   uint32_t n_ok = 0, n_alt = 0;
-
-  // kProbeRecs keys: skip the resolved ones (pass C), fetch all buckets, act
-  auto work = [&](const uint32_t (&idx)[kProbeRecs], const uint64_t (&bk)[kProbeRecs],
-                  const uint64_t (&fp)[kProbeRecs], bool (&go)[kProbeRecs]) {
+  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
+  for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
+    uint32_t r;
+    uint64_t off0;
+    tile_coords(s, pl, r, off0);
+    const uint32_t c = w.cnt1[(size_t)r * kCntStride];
+    const uint64_t cnt = c < pl.cap ? c : pl.cap;
+    if (off0 >= cnt) continue;  // block-uniform
+    const uint64_t* src = w.bin1 + r * pl.cap;
+    uint64_t rec[kTileItems];
+    uint32_t bin[kTileItems];
+    bool need[kTileItems];
 #pragma unroll
-    for (int q = 0; q < kProbeRecs; ++q) {
-      if (SECOND && go[q]) {  // already resolved by pass B?
-        go[q] = !((__ldcg(sk.bits + (idx[q] >> 5)) >> (idx[q] & 31)) & 1u);
-        n_alt += go[q];
+    for (int j0 = 0; j0 < kTileItems; j0 += kProbeItems) {
+      uint64_t fp[kProbeItems], i1[kProbeItems];
+      uint32_t idx[kProbeItems];
+      uint64_t wv[kProbeItems][WPB];
+      bool v[kProbeItems];
+#pragma unroll
+      for (int q = 0; q < kProbeItems; ++q) {
+        const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
+        v[q] = off < cnt;
+        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
+        unpack_rec(rc, r, pl, idx[q], i1[q], fp[q]);
+        if (v[q]) Lg::fetch(words, i1[q], wv[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kProbeItems; ++q) {
+        const int j = j0 + q;
+        const bool done = v[q] && Lg::act(words, i1[q], fp[q], fp[q], wv[q]);
+        if (done) {
+          ++n_ok;
+          if (OP != OP_INSERT) set_bit(sk.bits, idx[q]);
+        }
+        need[j] = v[q] && !done;
+        n_alt += need[j];
+        uint64_t cc;
+        const uint64_t i2 = alt_index<POL>(i1[q], fp[q], 0, g, cc);
+        bin[j] = bin_of(i2, pl);
+        rec[j] = pack_rec(idx[q], i2 - (uint64_t)bin[j] * pl.rb, fp[q], pl);
       }
     }
-    uint64_t wv[kProbeRecs][WPB];
-#pragma unroll
-    for (int q = 0; q < kProbeRecs; ++q)
-      if (go[q]) Lg::fetch(words, bk[q], wv[q]);
-    bool fail[kProbeRecs];
-#pragma unroll
-    for (int q = 0; q < kProbeRecs; ++q) {
-      const bool done = go[q] && Lg::act(words, bk[q], fp[q], SECOND ? Lg::tag2(fp[q], g) : fp[q], wv[q]);
-      fail[q] = go[q] && !done;
-      if (done) {
+    block_append(rec, bin, need, pl, w.bin2, w.cnt2, sm, [&](uint64_t rc, uint32_t r2) {
+      uint32_t ii;
+      uint64_t i2, fp;
+      unpack_rec(rc, r2, pl, ii, i2, fp);
+      if (Lg::second(words, i2, fp, g)) {
         ++n_ok;
-        if (OP != OP_INSERT || !SECOND) set_bit(sk.bits, idx[q]);
+        if (OP != OP_INSERT) set_bit(sk.bits, ii);
+      } else if (OP == OP_INSERT) {
+        const uint64_t k = sk.keys[ii];
+        enqueue_evict_one(sk, ii, sk.hashed ? k : xxh64(k, g.seed));
       }
-    }
-    if (OP == OP_INSERT && SECOND) {
-#pragma unroll
-      for (int q = 0; q < kProbeRecs; ++q) enqueue_evict(sk, fail[q], idx[q], g);
-    }
-  };
-
-  for (uint64_t p0 = gtid * kProbeRecs; p0 < total; p0 += nthreads * kProbeRecs) {
-    const uint32_t r = (uint32_t)(p0 / pl.cap);
-    const uint64_t off = p0 - (uint64_t)r * pl.cap;
-    const uint32_t c = cnt[(size_t)r * kCntStride];
-    const uint64_t lim = c < pl.cap ? c : pl.cap;
-    uint64_t rec[kProbeRecs];
-    if (off + kProbeRecs <= lim) {
-      asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
-                   : "=l"(rec[0]), "=l"(rec[1]), "=l"(rec[2]), "=l"(rec[3])
-                   : "l"(list + p0), "l"(pol));
-    } else {
-#pragma unroll
-      for (int q = 0; q < kProbeRecs; ++q) rec[q] = off + q < lim ? list[p0 + q] : ~0ull;
-    }
-    uint64_t fp[kProbeRecs], bk[kProbeRecs];
-    uint32_t idx[kProbeRecs];
-    bool go[kProbeRecs];
-#pragma unroll
-    for (int q = 0; q < kProbeRecs; ++q) {
-      go[q] = rec[q] != ~0ull;
-      unpack_rec(rec[q], r, pl, idx[q], bk[q], fp[q]);
-    }
-    work(idx, bk, fp, go);
-  }
-
-  // drain this pass's overflow list (keys whose bin was full)
-  const unsigned long long nov = *(volatile unsigned long long*)(w.novf + (SECOND ? 16 : 0));
-  const uint64_t* oh = w.ovf_h + (SECOND ? n : 0);
-  const uint32_t* ox = w.ovf_x + (SECOND ? n : 0);
-  for (uint64_t p0 = gtid * kProbeRecs; p0 < nov; p0 += nthreads * kProbeRecs) {
-    uint64_t fp[kProbeRecs], bk[kProbeRecs];
-    uint32_t idx[kProbeRecs];
-    bool go[kProbeRecs];
-#pragma unroll
-    for (int q = 0; q < kProbeRecs; ++q) {
-      go[q] = p0 + q < nov;
-      uint64_t i1 = 0, i2 = 0;
-      fp[q] = 1;
-      idx[q] = go[q] ? ox[p0 + q] : 0;
-      if (go[q]) place<POL>(oh[p0 + q], g, fp[q], i1, i2);
-      bk[q] = SECOND ? i2 : i1;
-    }
-    work(idx, bk, fp, go);
+    });
   }
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
+}
+
+// ---- pass C: alternate buckets ----
+
+template <int OP, int F, int WPB, int POL>
+__global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
+    tile_probe2_kernel(Geo g, Plan pl, uint64_t* words, Work w, Sink sk, long long* occ) {
+  using Lg = Logic<OP, F, WPB, POL>;
+  const uint64_t pol = evict_first_policy();
+  uint32_t n_ok = 0;
+  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
+  for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
+    uint32_t r;
+    uint64_t off0;
+    tile_coords(s, pl, r, off0);
+    const uint32_t c = w.cnt2[(size_t)r * kCntStride];
+    const uint64_t cnt = c < pl.cap ? c : pl.cap;
+    if (off0 >= cnt) continue;
+    const uint64_t* src = w.bin2 + r * pl.cap;
+#pragma unroll
+    for (int j0 = 0; j0 < kTileItems; j0 += kProbeItems) {
+      uint64_t fp[kProbeItems], i2[kProbeItems];
+      uint32_t idx[kProbeItems];
+      uint64_t wv[kProbeItems][WPB];
+      bool v[kProbeItems];
+#pragma unroll
+      for (int q = 0; q < kProbeItems; ++q) {
+        const uint64_t off = off0 + (j0 + q) * kTileThreads + threadIdx.x;
+        v[q] = off < cnt;
+        const uint64_t rc = v[q] ? ld_stream_ef(src + off, pol) : 0;
+        unpack_rec(rc, r, pl, idx[q], i2[q], fp[q]);
+        if (v[q]) Lg::fetch(words, i2[q], wv[q]);
+      }
+#pragma unroll
+      for (int q = 0; q < kProbeItems; ++q) {
+        const bool done = v[q] && Lg::act(words, i2[q], fp[q], Lg::tag2(fp[q], g), wv[q]);
+        if (done) {
+          ++n_ok;
+          if (OP != OP_INSERT) set_bit(sk.bits, idx[q]);
+        }
+        if (OP == OP_INSERT) enqueue_evict(sk, v[q] && !done, idx[q], g);
+      }
+    }
+  }
+  block_count_add(n_ok, 0, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
 // bitmap -> one byte per key
