@@ -319,19 +319,30 @@ def run_ours(args) -> None:
         del pos, neg
         torch.cuda.empty_cache()
 
+        debug = bool(os.environ.get("BENCH_DEBUG"))
+
         def e2e_step():
+            t = [time.perf_counter()]
             r = filt.insert_batch(pos_p)
             ok_h = r.ok  # D2H of the per-key results
+            t.append(time.perf_counter())
             q1 = filt.query_batch(pos_p)
+            t.append(time.perf_counter())
             q2 = filt.query_batch(neg_p)
+            t.append(time.perf_counter())
             dd = filt.delete_batch(pos_p)
+            t.append(time.perf_counter())
+            if debug:
+                print("e2e ms per op:", [round(1e3 * (b - a), 1) for a, b in zip(t, t[1:])], file=sys.stderr)
             return ok_h, q1, q2, dd
 
         e2e_step()
         barrier()
         t0 = time.perf_counter()
         ksteps = max(1, min(args.steps, args.e2e_steps))
+        out = None
         for _ in range(ksteps):
+            out = None  # release the previous step's host answers (their pinned blocks are reused)
             out = e2e_step()
         barrier()
         dt = (time.perf_counter() - t0) / ksteps
@@ -387,7 +398,7 @@ def main() -> None:
     ap.add_argument("--log2-slots", type=int, default=28)
     ap.add_argument("--eviction", choices=["dfs", "bfs"], default="bfs")
     ap.add_argument("--cpu-log2-slots", type=int, default=24)
-    ap.add_argument("--e2e-steps", type=int, default=3)
+    ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     args = ap.parse_args()

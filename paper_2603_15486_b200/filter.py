@@ -115,8 +115,29 @@ class BatchInsertResult:
         self._lost = None
         self._nrec = None
 
+    @classmethod
+    def from_parts(cls, n: int, ok_host: torch.Tensor, parts) -> "BatchInsertResult":
+        """Result of a chunked host pipeline: host ok + per-chunk records."""
+        self = cls.__new__(cls)
+        self._n = n
+        self._ok_dev = None
+        self._ok = ok_host
+        self._parts = parts
+        self._kind = "cpu"
+        self._numpy = False
+        self._ev = self._lost = None
+        self._nrec = None
+        return self
+
     # -- device-side summaries (one tiny D2H each) --
     def _counts(self):
+        if getattr(self, "_parts", None) is not None and self._nrec is None:
+            c = torch.stack([ctr for _, _, ctr in self._parts]).cpu()
+            self._nok_cached = int(c[:, 0].sum())
+            self._nrec = int(c[:, 1].sum())
+            self._nalt = int(c[:, 3].sum())
+            self._part_nrec = c[:, 1].tolist()
+            return self._nok_cached, self._nrec
         if self._nrec is None:
             c = self._ctr.cpu()
             self._nok_cached = int(c[0])
@@ -141,6 +162,13 @@ class BatchInsertResult:
     def records(self) -> np.ndarray:
         """The sparse (index, lost, evictions, ok) records, host structured array."""
         nrec = self._counts()[1]
+        if getattr(self, "_parts", None) is not None:
+            out = []
+            for (lo, rec, _), cnt in zip(self._parts, self._part_nrec):
+                r = rec[: cnt * _lib.RECORD_BYTES].cpu().numpy().view(_REC_DTYPE).copy()
+                r["index"] += lo
+                out.append(r)
+            return np.concatenate(out) if out else np.zeros(0, dtype=_REC_DTYPE)
         raw = self._rec[: nrec * _lib.RECORD_BYTES].cpu().numpy()
         return raw.view(_REC_DTYPE)
 
@@ -208,6 +236,7 @@ class CuckooFilter:
         # None: library heuristic; True: L2-tiled whenever applicable; False: direct kernels
         self._tiled_flags = {None: 0, True: _lib.FORCE_TILED, False: _lib.FORCE_DIRECT}[tiled]
         self._ws = None  # grow-only scratch for the L2-tiled path
+        self._pipe = None  # streams + chunk buffers of the host pipeline
         with torch.cuda.device(self.device):
             self.words_device = torch.zeros(cfg.total_words, dtype=torch.int64, device=self.device)
             # [0] occupancy (kernels add/subtract), [1..4] scratch counters for scalar ops
@@ -408,46 +437,130 @@ class CuckooFilter:
             if self._debug:
                 self._exit_mutate()
 
+    # ---- one C-ABI launch on device buffers (current stream) ----
+
+    def _launch(self, op: int, k: torch.Tensor, out: torch.Tensor, flags: int, p=None,
+                rec: Optional[torch.Tensor] = None, ctr: Optional[torch.Tensor] = None) -> None:
+        n = k.numel()
+        p = self._params if p is None else p
+        L = _lib.lib()
+        ws, wsb = self._workspace(p, n, op, flags)
+        if op == _lib.OP_INSERT:
+            _lib.check(L.ckf_insert(
+                ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, out.data_ptr(),
+                None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(), ws, wsb,
+                flags, self._stream()))
+        elif op == _lib.OP_QUERY:
+            _lib.check(L.ckf_query(
+                ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, out.data_ptr(),
+                self._ctr.data_ptr(), ws, wsb, flags, self._stream()))
+        else:
+            _lib.check(L.ckf_delete(
+                ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, out.data_ptr(),
+                self._ctr.data_ptr(), self._occ.data_ptr(), ws, wsb, flags, self._stream()))
+
+    # Host-resident batches larger than this stream through the GPU in chunks:
+    # chunk i+1 is copied in while chunk i is processed and chunk i-1's answers
+    # are copied out (PCIe is the bound for host data: ~55 GB/s each way).
+    HOST_CHUNK = 1 << 25
+
+    def _host_pipeline(self, op: int, keys: torch.Tensor, flags: int, p=None):
+        """Chunked H2D -> kernel -> D2H with copy/compute overlap for CPU keys.
+        Returns (host bool answers, [(offset, rec, ctr)] for insert)."""
+        n = keys.numel()
+        C = self.HOST_CHUNK
+        dev = self.device
+        comp = torch.cuda.current_stream(dev)
+        if self._pipe is None:
+            self._pipe = {
+                "in": torch.cuda.Stream(dev), "out": torch.cuda.Stream(dev),
+                "keys": [torch.empty(C, dtype=torch.int64, device=dev) for _ in range(2)],
+                "res": [torch.empty(C, dtype=torch.uint8, device=dev) for _ in range(2)],
+            }
+        P = self._pipe
+        ans = torch.empty(n, dtype=torch.bool, pin_memory=True)
+        parts = []
+        free_in, free_out = [None, None], [None, None]
+        for ci, lo in enumerate(range(0, n, C)):
+            hi, b = min(n, lo + C), ci & 1
+            m = hi - lo
+            with torch.cuda.stream(P["in"]):
+                if free_in[b] is not None:
+                    P["in"].wait_event(free_in[b])
+                P["keys"][b][:m].copy_(keys[lo:hi], non_blocking=True)
+                e_in = torch.cuda.Event()
+                e_in.record(P["in"])
+            comp.wait_event(e_in)
+            if free_out[b] is not None:
+                comp.wait_event(free_out[b])
+            rec = ctr = None
+            if op == _lib.OP_INSERT:
+                rec = torch.empty(m * _lib.RECORD_BYTES, dtype=torch.uint8, device=dev)
+                ctr = torch.empty(4, dtype=torch.int64, device=dev)
+                parts.append((lo, rec, ctr))
+            self._launch(op, P["keys"][b][:m], P["res"][b][:m], flags, p, rec, ctr)
+            e_c = torch.cuda.Event()
+            e_c.record(comp)
+            free_in[b] = e_c
+            with torch.cuda.stream(P["out"]):
+                P["out"].wait_event(e_c)
+                ans[lo:hi].copy_(P["res"][b][:m].view(torch.bool), non_blocking=True)
+                e_o = torch.cuda.Event()
+                e_o.record(P["out"])
+                free_out[b] = e_o
+        P["out"].synchronize()
+        return ans, parts
+
     def _insert(self, keys, worker: int, deterministic: Optional[bool], hashed: bool = False) -> BatchInsertResult:
+        p = self._params_for(worker)
+        flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
+        if self._chunkable(keys):
+            with torch.cuda.device(self.device):
+                ans, parts = self._host_pipeline(_lib.OP_INSERT, self._cpu_keys(keys), flags, p)
+            return BatchInsertResult.from_parts(keys.numel(), ans, parts)
         k, kind = self._as_keys(keys)
         n = k.numel()
         with torch.cuda.device(self.device):
             ok = torch.empty(n, dtype=torch.uint8, device=self.device)
             rec = torch.empty(max(n, 1) * _lib.RECORD_BYTES, dtype=torch.uint8, device=self.device)
             ctr = torch.empty(4, dtype=torch.int64, device=self.device)
-            p = self._params_for(worker)
-            flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
-            ws, wsb = self._workspace(p, n, _lib.OP_INSERT, flags)
-            _lib.check(_lib.lib().ckf_insert(
-                ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, ok.data_ptr(),
-                None, None, rec.data_ptr(), n, ctr.data_ptr(), self._occ.data_ptr(), ws, wsb,
-                flags, self._stream()))
+            self._launch(_lib.OP_INSERT, k, ok, flags, p, rec, ctr)
         return BatchInsertResult(n, ok, rec, ctr, kind)
 
     def _query(self, keys, hashed: bool = False):
+        flags = self._tiled_flags | (_lib.INPUT_HASHED if hashed else 0)
+        if self._chunkable(keys):
+            with torch.cuda.device(self.device):
+                return self._host_pipeline(_lib.OP_QUERY, self._cpu_keys(keys), flags)[0]
         k, kind = self._as_keys(keys)
-        n = k.numel()
         with torch.cuda.device(self.device):
-            out = torch.empty(n, dtype=torch.uint8, device=self.device)
-            flags = self._tiled_flags | (_lib.INPUT_HASHED if hashed else 0)
-            ws, wsb = self._workspace(self._params, n, _lib.OP_QUERY, flags)
-            _lib.check(_lib.lib().ckf_query(
-                ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
-                out.data_ptr(), self._ctr.data_ptr(), ws, wsb, flags, self._stream()))
+            out = torch.empty(k.numel(), dtype=torch.uint8, device=self.device)
+            self._launch(_lib.OP_QUERY, k, out, flags)
         return self._answer(out.view(torch.bool), kind)
 
     def _delete(self, keys, deterministic: Optional[bool], hashed: bool = False):
+        flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
+        if self._chunkable(keys) and not (flags & _lib.MODE_SEQUENTIAL):
+            with torch.cuda.device(self.device):
+                return self._host_pipeline(_lib.OP_DELETE, self._cpu_keys(keys), flags)[0]
         k, kind = self._as_keys(keys)
-        n = k.numel()
         with torch.cuda.device(self.device):
-            out = torch.empty(n, dtype=torch.uint8, device=self.device)
-            flags = self._flags(deterministic) | (_lib.INPUT_HASHED if hashed else 0)
-            ws, wsb = self._workspace(self._params, n, _lib.OP_DELETE, flags)
-            _lib.check(_lib.lib().ckf_delete(
-                ctypes.byref(self._params), self.words_device.data_ptr(), k.data_ptr(), n,
-                out.data_ptr(), self._ctr.data_ptr(), self._occ.data_ptr(), ws, wsb, flags,
-                self._stream()))
+            out = torch.empty(k.numel(), dtype=torch.uint8, device=self.device)
+            self._launch(_lib.OP_DELETE, k, out, flags)
         return self._answer(out.view(torch.bool), kind)
+
+    def _chunkable(self, keys) -> bool:
+        """Large host torch tensors take the overlapped chunked pipeline."""
+        return (isinstance(keys, torch.Tensor) and keys.device.type == "cpu" and keys.dim() == 1
+                and keys.numel() > self.HOST_CHUNK and not self._deterministic)
+
+    @staticmethod
+    def _cpu_keys(keys: torch.Tensor) -> torch.Tensor:
+        if keys.dtype == torch.uint64:
+            keys = keys.view(torch.int64)
+        elif keys.dtype != torch.int64:
+            keys = keys.to(torch.int64)
+        return keys.contiguous()
 
     def last_counters(self) -> dict:
         """Device counters of the last query / delete batch (one small D2H)."""
