@@ -412,7 +412,7 @@ __device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_
 // start from those snapshots.  Decisions are taken in exactly the reference
 // order (first candidate with room, K:407-414), so the sequential parity mode
 // stays bit-identical.
-constexpr int kEvictFetch = 4;
+constexpr int kEvictFetch = 2;
 
 template <int F>
 __device__ __forceinline__ bool lane_cas_from(uint64_t* p, int lane, uint64_t expect, uint64_t repl, uint64_t w) {
@@ -425,12 +425,34 @@ __device__ __forceinline__ bool lane_cas_from(uint64_t* p, int lane, uint64_t ex
   }
 }
 
+// word j of a register snapshot, selected without dynamic indexing (which
+// would put the snapshot in local memory)
+template <int WPB>
+__device__ __forceinline__ uint64_t snap_word(const uint64_t (&w)[WPB], uint32_t j) {
+  uint64_t r = w[0];
+#pragma unroll
+  for (int q = 1; q < WPB; ++q)
+    if (j == (uint32_t)q) r = w[q];
+  return r;
+}
+
+// BFS candidate order (K:257-272) without candidate arrays: the occupied
+// slots of the snapshot as a bit mask rotated to start at `start`; candidate
+// j is the slot of the j-th set bit.
+template <uint32_t B>
+__device__ __forceinline__ uint32_t nth_candidate(uint64_t rot, uint32_t j, uint32_t start) {
+  for (uint32_t k = 0; k < j; ++k) rot &= rot - 1;
+  uint32_t s = (uint32_t)(__ffsll((long long)rot) - 1) + start;
+  return s >= B ? s - B : s;
+}
+
 template <int F, int WPB, int POL>
 __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2, const Geo& g) {
   using L = Lanes<F>;
   constexpr int kTpw = L::kTpw;
   constexpr uint32_t kB = WPB * kTpw;
-  constexpr int kLim = kB / 2 ? kB / 2 : 1;
+  constexpr uint32_t kLim = kB / 2 ? kB / 2 : 1;
+  constexpr uint64_t kAll = kB == 64 ? ~0ull : ((1ull << kB) - 1u);
   const uint64_t tag2 = make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g);
   uint64_t st = rng_init(g.seed, h, g.worker) + kGolden;
   uint64_t cur_b = i1, cur_tag = fp;
@@ -459,44 +481,30 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
     uint64_t* base = words + cur_b * WPB;
     uint64_t cw[WPB];
     ld_bucket_rw<WPB>(base, cw);
-    // collect_candidates (K:257-272) from the snapshot
-    uint32_t cslot[kLim];
-    uint64_t ctag[kLim];
-    int cnt = 0;
+    uint64_t occ = 0;  // bit s = slot s occupied
 #pragma unroll
-    for (uint32_t j = 0; j < kB; ++j) {
-      uint32_t s = start + j;
-      if (s >= kB) s -= kB;
-      uint64_t word = cw[0];
+    for (int q = 0; q < WPB; ++q) {
+      const uint64_t z = L::zeros(cw[q]);
 #pragma unroll
-      for (int q = 1; q < WPB; ++q)
-        if ((int)(s / kTpw) == q) word = cw[q];
-      const uint64_t t = L::get(word, s % kTpw);
-      if (t && cnt < kLim) {
-#pragma unroll
-        for (int q = 0; q < kLim; ++q)
-          if (q == cnt) {
-            cslot[q] = s;
-            ctag[q] = t;
-          }
-        ++cnt;
-      }
+      for (int s = 0; s < kTpw; ++s)
+        if (!((z >> (s * F + F - 1)) & 1u)) occ |= 1ull << (q * kTpw + s);
     }
+    const uint64_t rot = start ? (((occ >> start) | (occ << (kB - start))) & kAll) : occ;
+    const uint32_t pc = (uint32_t)__popcll(rot);
+    const uint32_t cnt = pc < kLim ? pc : kLim;
     if (cnt == 0) {  // drained by concurrent deletes: take a direct slot
       if (try_insert_snap<F, WPB>(words, cur_b, cur_tag, cw) >= 0) return {1u, n, 0};
       continue;
     }
     int chosen = -1;
     uint64_t alt_b = 0, alt_tag = 0, aw_chosen[WPB];
-    for (int c0 = 0; c0 < cnt && chosen < 0; c0 += kEvictFetch) {
+    for (uint32_t c0 = 0; c0 < cnt && chosen < 0; c0 += kEvictFetch) {
       uint64_t aw[kEvictFetch][WPB], ab[kEvictFetch], at[kEvictFetch];
 #pragma unroll
       for (int q = 0; q < kEvictFetch; ++q) {
         if (c0 + q >= cnt) continue;
-        uint64_t ct = 0;
-#pragma unroll
-        for (int r = 0; r < kLim; ++r)
-          if (r == c0 + q) ct = ctag[r];
+        const uint32_t s = nth_candidate<kB>(rot, c0 + q, start);
+        const uint64_t ct = L::get(snap_word<WPB>(cw, s / kTpw), s % kTpw);
         uint64_t tc;
         const uint64_t cfp = tag_fp(ct, g);
         ab[q] = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, tc);
@@ -510,7 +518,7 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
 #pragma unroll
         for (int j = 0; j < WPB; ++j) any |= L::zeros(aw[q][j]);
         if (any) {
-          chosen = c0 + q;
+          chosen = (int)(c0 + q);
           alt_b = ab[q];
           alt_tag = at[q];
 #pragma unroll
@@ -518,18 +526,9 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
         }
       }
     }
-    uint32_t os = 0;
-    uint64_t otag = 0;
-#pragma unroll
-    for (int r = 0; r < kLim; ++r)
-      if (r == (chosen >= 0 ? chosen : cnt - 1)) {
-        os = cslot[r];
-        otag = ctag[r];
-      }
-    uint64_t ow = cw[0];
-#pragma unroll
-    for (int q = 1; q < WPB; ++q)
-      if ((int)(os / kTpw) == q) ow = cw[q];
+    const uint32_t os = nth_candidate<kB>(rot, chosen >= 0 ? (uint32_t)chosen : cnt - 1, start);
+    const uint64_t ow = snap_word<WPB>(cw, os / kTpw);
+    const uint64_t otag = L::get(ow, os % kTpw);
     if (chosen >= 0) {
       // two-step relocation: copy the candidate out, then swap ourselves in
       const int aslot = try_insert_snap<F, WPB>(words, alt_b, alt_tag, aw_chosen);

@@ -376,6 +376,8 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     const uint64_t cnt = c < pl.cap ? c : pl.cap;
     if (off0 >= cnt) continue;
     const uint64_t* src = w.bin2 + r * pl.cap;
+    uint32_t fidx[kTileItems];
+    uint32_t fmask = 0;
 #pragma unroll
     for (int j0 = 0; j0 < kTileItems; j0 += kProbeItems) {
       uint64_t fp[kProbeItems], i2[kProbeItems];
@@ -397,7 +399,32 @@ __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
           ++n_ok;
           if (OP != OP_INSERT) set_bit(sk.bits, idx[q]);
         }
-        if (OP == OP_INSERT) enqueue_evict(sk, v[q] && !done, idx[q], g);
+        fidx[j0 + q] = idx[q];
+        if (OP == OP_INSERT && v[q] && !done) fmask |= 1u << (j0 + q);
+      }
+    }
+    if (OP == OP_INSERT) {
+      // one queue reservation per warp per tile for all its unplaced keys
+      const int lane = threadIdx.x & 31;
+      const uint32_t c = __popc(fmask);
+      uint32_t incl = c;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+        if (lane >= d) incl += y;
+      }
+      const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+      unsigned long long base = 0;
+      if (lane == 31 && total) base = atomicAdd(&sk.ctr->n_queued, (unsigned long long)total);
+      base = __shfl_sync(0xffffffffu, base, 31);
+      uint64_t pos = base + incl - c;
+#pragma unroll
+      for (int j = 0; j < kTileItems; ++j) {
+        if (!((fmask >> j) & 1u)) continue;
+        const uint64_t k = sk.keys[fidx[j]];
+        if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{fidx[j], sk.hashed ? k : xxh64(k, g.seed), 0u, 0u};
+        else if (sk.ok) sk.ok[fidx[j]] = 0;
+        ++pos;
       }
     }
   }
