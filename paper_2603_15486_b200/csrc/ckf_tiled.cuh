@@ -34,7 +34,7 @@ constexpr int kTileThreads = 256;
 constexpr int kTileItems = 8;
 constexpr int kTile = kTileThreads * kTileItems;  // records per tile
 constexpr int kTileMinBlocks = 4;                  // >= 4 resident CTAs per SM (<= 64 registers)
-constexpr int kMaxBins = 1024;
+constexpr int kMaxBins = 512;
 constexpr int kCntStride = 32;                     // bin counters 128 B apart (one line each)
 constexpr int kProbeItems = 2;                     // bucket fetches in flight per thread
 
@@ -252,22 +252,55 @@ __device__ __forceinline__ void block_append(const uint64_t (&rec)[I], const uin
 
 // ---- pass A: hash + bin by primary-bucket region ----
 
+__device__ __forceinline__ void cp_async16(void* smem, const void* gmem, uint32_t src_bytes) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"((uint32_t)__cvta_generic_to_shared(smem)),
+               "l"(gmem), "r"(src_bytes)
+               : "memory");
+}
+
+// Stage tile [t0, t0 + kTile) of the keys into shared memory (zero-filled past
+// n); each thread copies its own 16-byte pieces, so no barrier is needed
+// before its own reads.
+__device__ __forceinline__ void stage_keys(uint64_t* buf, const uint64_t* keys, uint64_t t0, uint64_t n) {
+#pragma unroll
+  for (int q = 0; q < kTileItems / 2; ++q) {
+    const uint32_t e = (q * kTileThreads + threadIdx.x) * 2;  // element pair
+    const uint64_t i = t0 + e;
+    const uint32_t bytes = i + 2 <= n ? 16u : (i < n ? 8u : 0u);
+    cp_async16(buf + e, keys + (i < n ? i : 0), bytes);
+  }
+  asm volatile("cp.async.commit_group;" ::: "memory");
+}
+
 template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kTileThreads, kTileMinBlocks)
     tile_bin_kernel(Geo g, Plan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n, bool hashed,
                     Work w, Sink sk, long long* occ) {
   __shared__ SplitSmem sm;
+  __shared__ __align__(16) uint64_t kbuf[kTile];  // next tile's keys, copied in while this one is binned
   using Lg = Logic<OP, F, WPB, POL>;
   uint32_t n_ok = 0;
-  for (uint64_t t0 = blockIdx.x * (uint64_t)kTile; t0 < n; t0 += (uint64_t)gridDim.x * kTile) {
+  const uint64_t step = (uint64_t)gridDim.x * kTile;
+  uint64_t t0 = blockIdx.x * (uint64_t)kTile;
+  if (t0 < n) stage_keys(kbuf, keys, t0, n);
+  for (; t0 < n; t0 += step) {
     uint64_t rec[kTileItems];
     uint32_t bin[kTileItems];
     bool v[kTileItems];
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
+    uint64_t kk[kTileItems];
+#pragma unroll
+    for (int q = 0; q < kTileItems / 2; ++q) {  // the pairs this thread copied itself
+      const uint32_t e = (q * kTileThreads + threadIdx.x) * 2;
+      kk[2 * q] = kbuf[e];
+      kk[2 * q + 1] = kbuf[e + 1];
+    }
+    if (t0 + step < n) stage_keys(kbuf, keys, t0 + step, n);  // overlaps the rest of this tile
 #pragma unroll
     for (int j = 0; j < kTileItems; ++j) {
-      const uint64_t i = t0 + j * kTileThreads + threadIdx.x;
+      const uint64_t i = t0 + ((j >> 1) * kTileThreads + threadIdx.x) * 2 + (j & 1);
       v[j] = i < n;
-      const uint64_t h = v[j] ? load_hash(keys, i, g.seed, hashed) : 0;
+      const uint64_t h = hashed ? kk[j] : xxh64(kk[j], g.seed);
       uint64_t fp, i1, i2;
       place<POL>(h, g, fp, i1, i2);
       bin[j] = bin_of(i1, pl);
