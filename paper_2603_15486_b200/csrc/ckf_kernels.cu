@@ -402,7 +402,7 @@ static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags, bool& ok)
   pl.group = (uint32_t)env_u64("CKF_BIN_GROUP", 8);
   if (pl.group < 1) pl.group = 1;
   const double per = (double)n / (double)R;
-  pl.cap = (uint64_t)(per + 4.0 * std::sqrt(per) + 64.0);
+  pl.cap = ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + 1) & ~1ull;  // even: 16 B-aligned bins
   pl.tiles_per_bin = (uint32_t)((pl.cap + kTile - 1) / kTile);
   ok = true;
   return pl;
