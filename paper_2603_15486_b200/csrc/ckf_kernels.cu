@@ -32,6 +32,7 @@
 #include "ckf_semantics.cuh"
 #include "ckf_device.cuh"
 #include "ckf_tiled.cuh"
+#include "ckf_region.cuh"
 
 namespace ckf {
 
@@ -340,11 +341,15 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
 #define CKF_CASE_P(FF)                                        \
   if (p->policy == CKF_POLICY_XOR) { CKF_CASE_W(FF, 0) }      \
   else { CKF_CASE_W(FF, 1) }
+#ifdef CKF_DEV_F16  // developer build: f=16 only (fast compile)
+  if (p->fingerprint_bits == 16) { CKF_CASE_P(16) }
+#else
   switch (p->fingerprint_bits) {
     case 8: CKF_CASE_P(8)
     case 16: CKF_CASE_P(16)
     case 32: CKF_CASE_P(32)
   }
+#endif
 #undef CKF_CASE_P
 #undef CKF_CASE_W
   return CKF_EINVAL;
@@ -476,10 +481,177 @@ static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, ui
   return st;
 }
 
+// ---------------------------------------------------------------------------
+// shared-memory region schedule: plan + workspace layout (see ckf_region.cuh)
+// ---------------------------------------------------------------------------
+
+struct RLayout {
+  uint64_t cnt1, cntf, bin_ctr_end, n_miss, ctr_end, bin1, binf, miss, bits, total;
+};
+
+static uint32_t ceil_log2(uint64_t x) {
+  uint32_t l = 0;
+  while ((1ull << l) < x) ++l;
+  return l;
+}
+
+static uint64_t even_cap(double per) { return ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + 1) & ~1ull; }
+
+// Region plan; ok=false when the schedule does not apply to this table.
+static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags, bool& ok) {
+  RPlan pl{};
+  ok = false;
+  const uint32_t wpb = p->words_per_bucket;
+  if (wpb != 2 && wpb != 4 && wpb != 8) return pl;
+  const uint64_t m = p->bucket_count;
+  const uint32_t pb = p->payload_bits;
+  if (pb > 24 || m < 2 || m > (1ull << 32) || n == 0 || n >= 0xFFFFFFFFull) return pl;
+  const uint64_t bbytes = wpb * 8ull;
+  uint32_t lrb = 0;
+  const uint64_t smem = env_u64("CKF_REGION_KB", kRegionSmem >> 10) << 10;
+  while ((bbytes << (lrb + 1)) <= smem && (bbytes << (lrb + 1)) <= (uint64_t)kRegionSmem) ++lrb;
+  const uint32_t lm = ceil_log2(m);
+  if (flags & CKF_FORCE_TILED) {  // small forced tables still get >= 16 fine regions
+    const uint32_t cap = lm > 4 ? lm - 4 : 1;
+    if (lrb > cap) lrb = cap;
+  }
+  if (lrb < 1) lrb = 1;
+  if (lrb + pb > 31) lrb = 31 - pb;
+  // coarse regions: ~512 of them, at most 2^(31-pb) buckets each (record offset bits)
+  uint32_t lrbc = lm > 9 ? lm - 9 : 0;
+  if (lrbc < lrb) lrbc = lrb;
+  if (lrbc + pb > 31) lrbc = 31 - pb;
+  if (lrbc - lrb > 6) lrbc = lrb + 6;  // F2 <= 64
+  const uint64_t R1 = (m + (1ull << lrbc) - 1) >> lrbc;
+  if (R1 > (uint64_t)kRMaxCoarse) return pl;
+  pl.lrb = lrb;
+  pl.lrbc = lrbc;
+  pl.F2 = 1u << (lrbc - lrb);
+  pl.R1 = (uint32_t)R1;
+  pl.R = pl.R1 * pl.F2;
+  pl.pb = pb;
+  const double recs = (double)n;
+  (void)op;
+  pl.cap1 = even_cap(recs / pl.R1);
+  pl.capf = even_cap(recs / pl.R);
+  ok = true;
+  return pl;
+}
+
+constexpr uint32_t kMaxProbeGrid = 1024;
+
+// one persistent probe CTA per SM (fewer if there are fewer regions)
+static uint32_t probe_grid(const RPlan& pl) {
+  uint32_t gsz = (uint32_t)sm_count();
+  if (gsz > kMaxProbeGrid) gsz = kMaxProbeGrid;
+  return pl.R < gsz ? pl.R : gsz;
+}
+// a probe CTA's miss segment holds every record of its regions
+static uint64_t miss_seg(const RPlan& pl) {
+  const uint32_t gsz = probe_grid(pl);
+  return (uint64_t)((pl.R + gsz - 1) / gsz) * pl.capf;
+}
+
+static RLayout rlayout_for(const RPlan& pl, uint64_t n, int op) {
+  RLayout L{};
+  const uint64_t cs = (uint64_t)kCntStride * 4;
+  L.cnt1 = 0;
+  L.cntf = align256(L.cnt1 + pl.R1 * cs);
+  L.bin_ctr_end = align256(L.cntf + pl.R * cs);  // bin counters: zeroed again between the phases
+  L.n_miss = L.bin_ctr_end;
+  L.ctr_end = align256(L.n_miss + 4ull * kMaxProbeGrid);
+  L.bin1 = L.ctr_end;
+  L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
+  L.miss = align256(L.binf + pl.R * pl.capf * 8);
+  L.bits = align256(L.miss + probe_grid(pl) * miss_seg(pl) * 16);
+  L.total = align256(L.bits + (op == CKF_OP_INSERT ? 0 : (n + 31) / 32 * 4));
+  (void)op;
+  return L;
+}
+
+static RWork rwork_view(void* ws, const RLayout& L, const RPlan& pl) {
+  char* b = (char*)ws;
+  RWork w{};
+  w.cnt1 = (uint32_t*)(b + L.cnt1);
+  w.cntf = (uint32_t*)(b + L.cntf);
+  w.n_miss = (uint32_t*)(b + L.n_miss);
+  w.bin1 = (uint64_t*)(b + L.bin1);
+  w.binf = (uint64_t*)(b + L.binf);
+  w.miss = (uint4*)(b + L.miss);
+  w.bits = (uint32_t*)(b + L.bits);
+  w.seg = miss_seg(pl);
+  return w;
+}
+
+// Opt a kernel into > 48 KiB of dynamic shared memory, once per kernel
+// instance and device (the template parameter makes the flag per instance).
+template <auto Kernel>
+static void allow_big_smem(uint32_t bytes) {
+  static bool done[64] = {};
+  int dev = 0;
+  cudaGetDevice(&dev);
+  if (dev >= 0 && dev < 64 && !done[dev]) {
+    cudaFuncSetAttribute(Kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+    done[dev] = true;
+  }
+}
+
+// Region run of one op: bin, split, probe on the primary buckets; bin, split,
+// probe the misses on their alternate buckets; (+ bit expansion).
+template <int OP, int F, int WPB, int POL>
+static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws, uint64_t* words,
+                      const uint64_t* keys, uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out,
+                      cudaStream_t s) {
+  RWork w = rwork_view(ws, L, pl);
+  if (cudaMemsetAsync(ws, 0, L.ctr_end, s) != cudaSuccess) return cuda_error();  // bin + miss counters
+  if (OP != OP_INSERT) {
+    if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
+    sk.bits = w.bits;
+  }
+  sk.keys = keys;
+  sk.hashed = hashed;
+  long long* mocc = OP == OP_QUERY ? nullptr : occ;
+  const int sms = sm_count();
+  const unsigned pg = probe_grid(pl);
+  constexpr uint32_t kBinSmem = sizeof(BinSmem);
+  allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
+  allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
+  allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmem);
+  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmem);
+  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
+  int st;
+  // phase 1: primary buckets
+  region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, 3), kBThreads, kBinSmem, s>>>(
+      g, pl, words, keys, n, hashed, w, sk, mocc);
+  if ((st = status())) return st;
+  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
+  if ((st = status())) return st;
+  region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
+  if ((st = status())) return st;
+  // phase 2: the misses, on their alternate buckets
+  if (cudaMemsetAsync(ws, 0, L.bin_ctr_end, s) != cudaSuccess) return cuda_error();
+  region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * 3 + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
+      g, pl, words, keys, 0, hashed, w, sk, mocc);
+  if ((st = status())) return st;
+  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
+  if ((st = status())) return st;
+  region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
+  if ((st = status())) return st;
+  if (OP != OP_INSERT) {
+    expand_count_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out,
+                                                                       OP == OP_QUERY ? sk.ctr : nullptr);
+    st = status();
+  }
+  return st;
+}
+
 struct TiledArgs {
-  bool on;
+  bool on;      // L2-tiled schedule (ckf_tiled.cuh)
+  bool region;  // shared-memory region schedule (ckf_region.cuh)
   Plan pl;
   Layout L;
+  RPlan rpl;
+  RLayout RL;
   void* ws;
 };
 
@@ -498,7 +670,12 @@ struct QueryArgs {
 template <int F, int WPB, int POL>
 struct QueryOp {
   static int run(const QueryArgs& a) {
-    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+      if (a.t.region) {
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
+        return run_region<OP_QUERY, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
+                                                 a.n, a.hashed, sk, nullptr, a.out, a.s);
+      }
       if (a.t.on) {
         Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
         return run_tiled<OP_QUERY, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
@@ -540,8 +717,17 @@ struct InsertOp {
     }
     int st = CKF_OK;
     bool tiled = false;
-    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
-      if (a.t.on && a.cap) {
+    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+      if (a.t.region && a.cap) {
+        tiled = true;
+        if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
+        if (a.ev && cudaMemsetAsync(a.ev, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
+        if (a.lost && cudaMemsetAsync(a.lost, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
+        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, nullptr, false};
+        st = run_region<OP_INSERT, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
+                                                a.occ, nullptr, a.s);
+        if (st) return st;
+      } else if (a.t.on && a.cap) {
         tiled = true;
         // every key counts as stored until the eviction pass says otherwise
         if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
@@ -592,7 +778,12 @@ struct DeleteOp {
       seq_delete_kernel<F, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.occ, a.hashed);
       return status();
     }
-    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+      if (a.t.region) {
+        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
+        return run_region<OP_DELETE, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
+                                                  a.occ, a.out, a.s);
+      }
       if (a.t.on) {
         Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
         return run_tiled<OP_DELETE, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
@@ -692,13 +883,29 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
 
 // Decide tiled vs direct for one call: tiled needs the plan to apply and a
 // large enough caller workspace.
-static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, void* ws, uint64_t ws_bytes) {
+// Developer knob: CKF_SCHED=l2 selects the L2-tiled schedule instead of the
+// shared-memory region schedule (both are legal concurrent schedules).
+static bool use_region() {
+  const char* v = getenv("CKF_SCHED");
+  return !(v && v[0] == 'l');
+}
+
+static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys, void* ws,
+                        uint64_t ws_bytes) {
   TiledArgs t{};
   if (!ws || !tiled_applies(p, n, flags)) return t;
-  bool ok;
+  t.ws = ws;
+  bool ok = false;
+  if (use_region() && ((uintptr_t)keys % 16) == 0) {
+    t.rpl = make_rplan(p, n, op, flags, ok);
+    if (ok) {
+      t.RL = rlayout_for(t.rpl, n, op);
+      t.region = ws_bytes >= t.RL.total && ((uintptr_t)ws % 256) == 0;
+      if (t.region) return t;
+    }
+  }
   t.pl = make_plan(p, n, flags, ok);
   t.L = layout_for(t.pl, n, op);
-  t.ws = ws;
   t.on = ws_bytes >= t.L.total && ((uintptr_t)ws % 256) == 0;
   return t;
 }
@@ -706,7 +913,15 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
   if (!params_ok(p) || !tiled_applies(p, n, flags)) return 0;
   bool ok;
-  return layout_for(make_plan(p, n, flags, ok), n, op).total;
+  uint64_t need = layout_for(make_plan(p, n, flags, ok), n, op).total;
+  if (use_region()) {
+    const RPlan rp = make_rplan(p, n, op, flags, ok);
+    if (ok) {
+      const uint64_t r = rlayout_for(rp, n, op).total;
+      if (r > need) need = r;
+    }
+  }
+  return need;
 }
 
 int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* ok, int64_t* evictions,
@@ -719,7 +934,7 @@ int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   if (!keys || !ok || (record_cap && !records)) return CKF_EINVAL;
   InsertArgs a{geo_from(*p), words, keys, n, ok, evictions, lost, records, records ? record_cap : 0,
                counters, occupancy, (flags & CKF_INPUT_HASHED) != 0, (flags & CKF_MODE_SEQUENTIAL) != 0, s,
-               choose(p, n, CKF_OP_INSERT, flags, workspace, workspace_bytes)};
+               choose(p, n, CKF_OP_INSERT, flags, keys, workspace, workspace_bytes)};
   return dispatch3<InsertOp>(p, words, a);
 }
 
@@ -731,7 +946,7 @@ int ckf_query(const ckf_params* p, const uint64_t* words, const uint64_t* keys, 
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
   QueryArgs a{geo_from(*p), words, keys, n, out, counters, (flags & CKF_INPUT_HASHED) != 0, s,
-              choose(p, n, CKF_OP_QUERY, flags, workspace, workspace_bytes)};
+              choose(p, n, CKF_OP_QUERY, flags, keys, workspace, workspace_bytes)};
   return dispatch3<QueryOp>(p, words, a);
 }
 
@@ -744,7 +959,7 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   if (n == 0) return CKF_OK;
   if (!keys || !out) return CKF_EINVAL;
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,
-               (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, workspace, workspace_bytes)};
+               (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, keys, workspace, workspace_bytes)};
   return dispatch3<DeleteOp>(p, words, a);
 }
 

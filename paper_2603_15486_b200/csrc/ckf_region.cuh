@@ -1,0 +1,784 @@
+// ckf_region.cuh -- shared-memory region schedule for large batches.
+//
+// Why (measured, profiles/r01s2_*): a bucket access that misses L2 costs a
+// random HBM row activation (~48 G sectors/s at 512 MiB, a quarter of the
+// streaming rate), and even an L2-resident one is bounded by the L2's random
+// request rate (~265 G loads/s, ~120 G CAS/s).  The L2-tiled schedule in
+// ckf_tiled.cuh got the buckets into L2 but stayed bound by those request
+// rates.  This schedule moves every bucket access into shared memory:
+//
+//   bin      hash + placement, records binned by COARSE table region of the
+//            key's primary bucket (R1 <= 512 bins);
+//   split    each coarse bin is split into F2 FINE bins (R = R1*F2 regions of
+//            rb buckets, rb*bucket_bytes <= 128 KiB);
+//   probe    one persistent CTA per SM takes fine regions in turn: the region's
+//            table slice is bulk-copied (TMA, cp.async.bulk) into shared memory,
+//            the region's records stream through a shared-memory ring of
+//            bulk-copied chunks, every op runs on the shared-memory copy
+//            (atom.shared.cas for mutations), and the slice is bulk-copied back;
+//   phase 2  keys their primary bucket did not answer (not found / full /
+//            tag absent) are appended to per-CTA dense miss lists during the
+//            probe, binned + split again by their alternate bucket and probed
+//            again; inserts still unplaced go to the eviction pass.
+// Every DRAM stream is sequential.  All bucket reads and CASes hit shared
+// memory.  Concurrency semantics are unchanged: one legal concurrent schedule
+// of the batch in which every key tries i1 before i2 (K:355-362); a region is
+// owned by exactly one CTA while it is resident, so the shared-memory copy is
+// the only copy being mutated.
+#pragma once
+
+#include "ckf_tiled.cuh"
+
+namespace ckf {
+
+// ---------------------------------------------------------------------------
+// async-proxy primitives: mbarriers and 1-D bulk copies (TMA)
+// ---------------------------------------------------------------------------
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, 1000000;\n\t"
+      "@!p bra WAIT_%=;\n}\n" ::"r"(saddr(b)),
+      "r"(parity)
+      : "memory");
+}
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                   saddr(dst)),
+               "l"(src), "r"(bytes), "r"(saddr(bar))
+               : "memory");
+}
+__device__ __forceinline__ void bulk_s2g(void* dst, const void* src, uint32_t bytes) {
+  asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst), "r"(saddr(src)), "r"(bytes)
+               : "memory");
+  asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+__device__ __forceinline__ void bulk_wait_read() { asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory"); }
+__device__ __forceinline__ void bulk_wait_all() { asm volatile("cp.async.bulk.wait_group 0;" ::: "memory"); }
+__device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }
+__device__ __forceinline__ void fence_mbar_init() { asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory"); }
+__device__ __forceinline__ void prefetch_l2(const void* p, uint32_t bytes) {
+  asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+
+// ---------------------------------------------------------------------------
+// shared-memory bucket operations (same decisions as the global ones in
+// ckf_device.cuh: TryInsert K:158-180, TryRemove K:202-221, Find K:183-199)
+// ---------------------------------------------------------------------------
+
+template <int WPB>
+__device__ __forceinline__ void lds_bucket(uint32_t a, uint64_t (&w)[WPB]) {
+  if constexpr (WPB == 1) {
+    asm volatile("ld.shared.u64 %0, [%1];" : "=l"(w[0]) : "r"(a) : "memory");
+  } else {
+#pragma unroll
+    for (int s = 0; s < WPB / 2; ++s)
+      asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(w[2 * s]), "=l"(w[2 * s + 1]) : "r"(a + 16 * s) : "memory");
+  }
+}
+
+__device__ __forceinline__ uint64_t cas_shared(uint32_t a, uint64_t cmp, uint64_t val) {
+  uint64_t old;
+  asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(val) : "memory");
+  return old;
+}
+
+// ---- 32-bit SWAR on shared-memory snapshots ----
+// A lane never carries into its neighbour in ((x & ~H) + ~H), so each 32-bit
+// half of a word is handled on its own: exact per-lane zero indicators
+// (the carry-out form of W:9-16) in 3 ops per half.
+template <int F>
+__device__ __forceinline__ uint32_t zind32(uint32_t x) {
+  constexpr uint32_t H = (uint32_t)Lanes<F>::kHigh;
+  return ~(((x & ~H) + ~H) | x) & H;
+}
+// bit s of the result <=> lane s of x is zero (F = 8 or 16)
+template <int F>
+__device__ __forceinline__ uint32_t lane_mask(uint64_t x) {
+  const uint32_t zl = zind32<F>((uint32_t)x), zh = zind32<F>((uint32_t)(x >> 32));
+  // indicators at bit 7 of bytes 0..3 -> bits 28..31 (no carries: all partial
+  // products land on distinct bits)
+  if constexpr (F == 16) {
+    return (__byte_perm(zl, zh, 0x7531) * 0x00204081u) >> 28;
+  } else {
+    return ((zl * 0x00204081u) >> 28) | (((zh * 0x00204081u) >> 28) << 4);
+  }
+}
+
+// Any lane of the bucket equal to fp (payload-only compare for the offset
+// policy, K:451-453).  (x - L) & ~x & H is nonzero iff some lane of x is zero:
+// exact for the boolean.  32-bit halves are tested on
+// their own (still exact).
+template <int F, int WPB, int POL>
+__device__ __forceinline__ bool match_any(const uint64_t (&w)[WPB], uint64_t fp) {
+  using L = Lanes<F>;
+  constexpr uint32_t H = (uint32_t)L::kHigh, Lo = (uint32_t)L::kLow;
+  constexpr uint32_t keep = POL == CKF_POLICY_OFFSET ? ~H : ~0u;
+  const uint32_t pat = (uint32_t)L::bcast(fp);
+  uint32_t acc = 0;
+#pragma unroll
+  for (int j = 0; j < WPB; ++j) {
+    const uint32_t a = ((uint32_t)w[j] & keep) ^ pat, b = ((uint32_t)(w[j] >> 32) & keep) ^ pat;
+    acc |= ((a - Lo) & ~a) | ((b - Lo) & ~b);
+  }
+  return (acc & H) != 0;
+}
+
+// kB-bit mask over the bucket's slots (slot = word * tpw + lane) of lanes equal
+// to `pat` (pat = 0: empty lanes)
+template <int F, int WPB>
+__device__ __forceinline__ uint64_t slot_mask(const uint64_t (&w)[WPB], uint64_t pat) {
+  constexpr int kTpw = 64 / F;
+  uint64_t m = 0;
+#pragma unroll
+  for (int j = 0; j < WPB; ++j) m |= (uint64_t)lane_mask<F>(w[j] ^ pat) << (j * kTpw);
+  return m;
+}
+
+// First slot of `m` in the reference scan order: words from `start` wrapping,
+// lowest lane first (K:166-179, K:207-220).  -1 if none.
+template <int F, int WPB>
+__device__ __forceinline__ int first_slot(uint64_t m, int start) {
+  constexpr int kTpw = 64 / F, kB = WPB * kTpw;
+  const int sh = start * kTpw;
+  uint64_t rot;
+  if constexpr (kB == 64) rot = sh ? (m >> sh) | (m << (64 - sh)) : m;
+  else rot = ((m >> sh) | (m << (kB - sh))) & ((1ull << kB) - 1u);
+  if (!rot) return -1;
+  const int f = __ffsll((long long)rot) - 1 + sh;
+  return f >= kB ? f - kB : f;
+}
+
+template <int WPB>
+__device__ __forceinline__ uint64_t pick(const uint64_t (&w)[WPB], int j) {
+  uint64_t r = w[0];
+#pragma unroll
+  for (int q = 1; q < WPB; ++q)
+    if (j == q) r = w[q];
+  return r;
+}
+
+// TryInsert on a shared-memory bucket (a = its shared address, w = snapshot).
+// A lost CAS reloads the bucket and decides again.
+template <int F, int WPB>
+__device__ __forceinline__ bool smem_insert(uint32_t a, uint64_t tag, uint64_t (&w)[WPB]) {
+  constexpr int kTpw = 64 / F, kB = WPB * kTpw;
+  const int start = (int)(tag % kB) / kTpw;
+  while (true) {
+    const int slot = first_slot<F, WPB>(slot_mask<F, WPB>(w, 0), start);
+    if (slot < 0) return false;
+    const int j = slot / kTpw, lane = slot % kTpw;
+    const uint64_t bw = pick<WPB>(w, j);
+    if (cas_shared(a + 8u * j, bw, bw | (tag << (lane * F))) == bw) return true;
+    lds_bucket<WPB>(a, w);
+  }
+}
+
+// TryRemove on a shared-memory bucket: full-lane match (K:476-480).
+template <int F, int WPB>
+__device__ __forceinline__ bool smem_remove(uint32_t a, uint64_t tag, uint64_t (&w)[WPB]) {
+  constexpr int kTpw = 64 / F, kB = WPB * kTpw;
+  const int start = (int)(tag % kB) / kTpw;
+  const uint64_t pat = Lanes<F>::bcast(tag);
+  while (true) {
+    const int slot = first_slot<F, WPB>(slot_mask<F, WPB>(w, pat), start);
+    if (slot < 0) return false;
+    const int j = slot / kTpw, lane = slot % kTpw;
+    const uint64_t bw = pick<WPB>(w, j);
+    if (cas_shared(a + 8u * j, bw, bw & ~(Lanes<F>::kLaneMask << (lane * F))) == bw) return true;
+    lds_bucket<WPB>(a, w);
+  }
+}
+
+// ---------------------------------------------------------------------------
+// plan, records, workspace
+// ---------------------------------------------------------------------------
+
+constexpr int kRegionSmem = 128 * 1024;  // table bytes of one fine region in shared memory
+constexpr int kRMaxCoarse = 512;
+
+// Record (8 B): index:32 | alt:1 | bucket offset in its region << pb | fp.
+// `alt` marks a record of the key's alternate bucket.
+struct RPlan {
+  uint64_t cap1;     // record slots per coarse bin (even)
+  uint64_t capf;     // record slots per fine bin (even)
+  uint32_t R1;       // coarse bins
+  uint32_t lrbc;     // log2 buckets per coarse region
+  uint32_t F2;       // fine regions per coarse region
+  uint32_t lrb;      // log2 buckets per fine region
+  uint32_t R;        // fine regions = R1 * F2 (the last ones may be empty)
+  uint32_t pb;       // fingerprint bits in a record
+};
+
+__device__ __forceinline__ uint64_t rpack(uint64_t idx, uint32_t alt, uint64_t off, uint64_t fp, uint32_t pb) {
+  return (idx << 32) | ((uint64_t)alt << 31) | (off << pb) | fp;
+}
+
+struct RWork {
+  uint32_t* cnt1;   // [R1 * kCntStride] coarse bin fill
+  uint32_t* cntf;   // [R * kCntStride] fine bin fill
+  uint64_t* bin1;   // [R1 * cap1] coarse bins
+  uint64_t* binf;   // [R * capf] fine bins
+  uint4* miss;      // [grid * seg] per-probe-CTA dense segments of phase-1 misses {idx, fp, i2 lo, i2 hi}
+  uint32_t* n_miss; // [grid] entries per segment
+  uint64_t seg;     // entries per segment
+  uint32_t* bits;   // [ceil(n/32)] result bitmap (query / delete)
+};
+
+// What to do with a record that finds its bin full (adversarial inputs only):
+// resolve it in place on the global table -- legal here because no region is
+// resident in shared memory while the bin / split kernels run.
+template <int OP, int F, int WPB, int POL>
+__device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, uint64_t rec, uint64_t bucket,
+                                               const Sink& sk, uint32_t& n_ok, uint32_t& n_alt) {
+  using Lg = Logic<OP, F, WPB, POL>;
+  const uint32_t idx = (uint32_t)(rec >> 32);
+  const uint64_t fp = rec & ((1ull << g.payload_bits) - 1u);
+  const bool phase2 = (rec >> 31) & 1u;  // the record is of the key's alternate bucket
+  uint64_t c;
+  bool done;
+  if (phase2) {
+    done = Lg::second(words, bucket, fp, g);
+  } else {
+    done = Lg::first(words, bucket, fp, g);
+    if (!done) {
+      ++n_alt;
+      done = Lg::second(words, alt_index<POL>(bucket, fp, 0, g, c), fp, g);
+    }
+  }
+  if (done) {
+    if (OP != OP_QUERY) ++n_ok;
+    if (OP != OP_INSERT) set_bit(sk.bits, idx);
+  } else if (OP == OP_INSERT) {
+    const uint64_t k = sk.keys[idx];
+    enqueue_evict_one(sk, idx, sk.hashed ? k : xxh64(k, g.seed));
+  }
+}
+
+// ---------------------------------------------------------------------------
+// bin: hash + placement, binned by coarse region (block counting sort, one
+// global reservation per (tile, bin), contiguous runs out)
+// ---------------------------------------------------------------------------
+
+constexpr int kBThreads = 256;
+constexpr int kBItems = 16;
+constexpr int kBTile = kBThreads * kBItems;  // records per tile
+constexpr uint32_t kNoSlot = 0xFFFFFFFFu;    // the record's bin is full
+
+struct BinSmem {
+  uint64_t rec[kBTile];
+  uint32_t dst[kBTile];   // destination slot (bin * cap + offset), or kNoSlot
+  uint32_t hist[kRMaxCoarse];  // counts, then exclusive starts
+  uint32_t off[kRMaxCoarse];   // global run base - start (mod 2^32)
+  uint32_t warp_sums[kBThreads / 32];
+};
+
+// counts in sm.hist -> exclusive starts in sm.hist, global bases - start in sm.off
+__device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem& sm) {
+  constexpr int NW = kBThreads / 32;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint32_t per = (nb + kBThreads - 1) / kBThreads;  // <= 2
+  const uint32_t lo = min(tid * per, nb), hi = min(lo + per, nb);
+  uint32_t c[2], gb[2], sum = 0;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t r = lo + k;
+    c[k] = r < hi ? sm.hist[r] : 0u;
+    gb[k] = c[k] ? atomicAdd(gcnt + (size_t)r * kCntStride, c[k]) : 0u;
+    sum += c[k];
+  }
+  uint32_t x = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) sm.warp_sums[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint32_t v = lane < NW ? sm.warp_sums[lane] : 0, s = v;
+#pragma unroll
+    for (int d = 1; d < NW; d <<= 1) {
+      const uint32_t y = __shfl_up_sync(0xffffffffu, s, d);
+      if (lane >= d) s += y;
+    }
+    if (lane < NW) sm.warp_sums[lane] = s - v;
+  }
+  __syncthreads();
+  uint32_t run = sm.warp_sums[wid] + x - sum;
+#pragma unroll
+  for (int k = 0; k < 2; ++k) {
+    const uint32_t r = lo + k;
+    if (r < hi) {
+      sm.hist[r] = run;
+      sm.off[r] = gb[k] - run;
+      run += c[k];
+    }
+  }
+}
+
+// Places record `rc` of bin b at its sorted tile position p, with its
+// destination slot (bins are laid out bin * cap + offset; < 2^32 slots).
+__device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc, uint64_t cap) {
+  const uint32_t p = sm.hist[b] + rank;
+  const uint32_t o = sm.off[b] + p;  // offset inside the bin
+  sm.rec[p] = rc;
+  sm.dst[p] = o < cap ? b * (uint32_t)cap + o : kNoSlot;
+}
+
+// Writes the tile's sorted records (`total` of them) to their slots; records
+// whose bin is full go to ovf(rec, p).
+template <class Ovf>
+__device__ __forceinline__ void bin_write(uint32_t total, uint64_t* __restrict__ out, BinSmem& sm, uint64_t pol,
+                                          Ovf&& ovf) {
+  for (uint32_t p = threadIdx.x; p < total; p += kBThreads) {
+    const uint32_t d = sm.dst[p];
+    const uint64_t rc = sm.rec[p];
+    if (d != kNoSlot) st_stream_ef(out + d, rc, pol);
+    else ovf(rc, p);
+  }
+}
+
+// SRC_KEYS: the batch's keys (or hashes), one record per key for its primary
+// bucket.  SRC_MISS: phase-1 misses {idx, fp, i2} from probe-CTA segment
+// blockIdx.y, one record for the alternate bucket.
+enum { SRC_KEYS = 0, SRC_MISS = 1 };
+
+template <int OP, int F, int WPB, int POL, int SRC>
+__global__ void __launch_bounds__(kBThreads, 3)
+    region_bin_kernel(Geo g, RPlan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n_keys, bool hashed,
+                      RWork w, Sink sk, long long* occ) {
+  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
+  BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
+  constexpr int KT = kBTile;  // items per tile
+  const uint64_t pol = evict_first_policy();
+  const uint32_t lmask = (1u << pl.lrbc) - 1u;
+  const uint64_t n = SRC == SRC_KEYS ? n_keys : w.n_miss[blockIdx.y];
+  const uint4* ms = w.miss + (uint64_t)blockIdx.y * w.seg;
+  uint32_t n_ok = 0, n_alt = 0;
+  for (uint64_t t0 = blockIdx.x * (uint64_t)KT; t0 < n; t0 += (uint64_t)gridDim.x * KT) {
+    if (threadIdx.x == 0) {
+      const uint64_t nx = t0 + (uint64_t)gridDim.x * KT;
+      if (nx < n && n - nx >= 2) {
+        if (SRC == SRC_KEYS) prefetch_l2(keys + nx, (uint32_t)(min((uint64_t)KT, n - nx) * 8) & ~15u);
+        else prefetch_l2(ms + nx, (uint32_t)min((uint64_t)KT, n - nx) * 16);
+      }
+    }
+    for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.hist[r] = 0;
+    uint64_t rec[kBItems];
+    uint32_t pk[kBItems];  // bin << 16 | rank; 0xFFFFFFFF = no record
+    if constexpr (SRC == SRC_KEYS) {
+      uint64_t kk[kBItems];
+#pragma unroll
+      for (int q = 0; q < kBItems / 2; ++q) {
+        const uint64_t i = t0 + (uint64_t)q * 2 * kBThreads + 2 * threadIdx.x;
+        if (i + 1 < n) {
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                       : "=l"(kk[2 * q]), "=l"(kk[2 * q + 1])
+                       : "l"(keys + i), "l"(pol));
+        } else {
+          kk[2 * q] = i < n ? keys[i] : 0;
+          kk[2 * q + 1] = 0;
+        }
+      }
+      __syncthreads();
+#pragma unroll
+      for (int q = 0; q < kBItems; ++q) {
+        const uint64_t i = t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
+        const uint64_t h = hashed ? kk[q] : xxh64(kk[q], g.seed);
+        const uint64_t fp0 = (h >> 32) & ((1ull << g.payload_bits) - 1u);
+        const uint64_t fp = fp0 ? fp0 : 1u;
+        const uint64_t i1 = reduce_index(h & 0xFFFFFFFFull, g);
+        const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
+        rec[q] = rpack(i, 0u, i1 & lmask, fp, pl.pb);
+        pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.hist[b1], 1u) : 0xFFFFFFFFu;
+      }
+    } else {
+      __syncthreads();  // hist zeroed
+#pragma unroll
+      for (int q0 = 0; q0 < kBItems; q0 += 4) {  // 4 entries (64 B) in flight per thread
+        uint4 e[4];
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t i = t0 + (uint64_t)(q0 + q) * kBThreads + threadIdx.x;
+          e[q] = i < n ? ms[i] : make_uint4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint64_t i = t0 + (uint64_t)(q0 + q) * kBThreads + threadIdx.x;
+          const uint64_t i2 = (uint64_t)e[q].z | ((uint64_t)e[q].w << 32);
+          const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
+          rec[q0 + q] = rpack(e[q].x, 1u, i2 & lmask, e[q].y, pl.pb);
+          pk[q0 + q] = i < n ? (b2 << 16) | atomicAdd(&sm.hist[b2], 1u) : 0xFFFFFFFFu;
+        }
+      }
+    }
+    __syncthreads();
+    bin_reserve(pl.R1, w.cnt1, sm);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kBItems; ++q)
+      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
+    __syncthreads();
+    const uint32_t total = (uint32_t)min((uint64_t)KT, n - t0);
+    bin_write(total, w.bin1, sm, pol, [&](uint64_t rc, uint32_t p) {
+      // the bin of sorted position p: the last bin whose start is <= p
+      uint32_t lo = 0, hi = pl.R1 - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (sm.hist[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      const uint64_t bucket = ((uint64_t)lo << pl.lrbc) + ((rc >> pl.pb) & lmask);
+      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
+    });
+    __syncthreads();
+  }
+  block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
+}
+
+// ---------------------------------------------------------------------------
+// split: coarse bin -> F2 fine bins (records re-based to the fine region)
+// ---------------------------------------------------------------------------
+
+template <int OP, int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBThreads, 3)
+    region_split_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
+  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
+  BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
+  const uint64_t pol = evict_first_policy();
+  const uint32_t tiles_per_bin = (uint32_t)((pl.cap1 + kBTile - 1) / kBTile);
+  const uint64_t tiles = (uint64_t)pl.R1 * tiles_per_bin;
+  const uint32_t fshift = pl.pb + pl.lrb;  // offset bits above the fine offset
+  const uint32_t fmask = pl.F2 - 1u;
+  const uint64_t keep = ~((uint64_t)((1u << (pl.lrbc - pl.lrb)) - 1u) << fshift);  // clears the fine-region bits
+  uint32_t n_ok = 0, n_alt = 0;
+  for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
+    const uint32_t c = (uint32_t)(s / tiles_per_bin);
+    const uint64_t off0 = (s % tiles_per_bin) * (uint64_t)kBTile;
+    const uint32_t cc = w.cnt1[(size_t)c * kCntStride];
+    const uint64_t cnt = cc < pl.cap1 ? cc : pl.cap1;
+    if (off0 >= cnt) continue;  // block-uniform
+    for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.hist[r] = 0;
+    const uint64_t* src = w.bin1 + c * pl.cap1 + off0;
+    const uint32_t nrec = (uint32_t)min((uint64_t)kBTile, cnt - off0);
+    uint64_t rec[kBItems];
+#pragma unroll
+    for (int q = 0; q < kBItems / 2; ++q) {
+      const uint32_t e = q * 2 * kBThreads + 2 * threadIdx.x;
+      if (e + 1 < nrec) {
+        asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
+                     : "=l"(rec[2 * q]), "=l"(rec[2 * q + 1])
+                     : "l"(src + e), "l"(pol));
+      } else {
+        rec[2 * q] = e < nrec ? src[e] : 0;
+        rec[2 * q + 1] = 0;
+      }
+    }
+    __syncthreads();
+    uint32_t pk[kBItems];
+#pragma unroll
+    for (int q = 0; q < kBItems; ++q) {
+      const uint32_t e = (q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
+      const uint32_t f = (uint32_t)(rec[q] >> fshift) & fmask;
+      pk[q] = e < nrec ? (f << 16) | atomicAdd(&sm.hist[f], 1u) : 0xFFFFFFFFu;
+    }
+    __syncthreads();
+    bin_reserve(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
+    __syncthreads();
+#pragma unroll
+    for (int q = 0; q < kBItems; ++q)
+      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
+    __syncthreads();
+    bin_write(nrec, w.binf + (uint64_t)c * pl.F2 * pl.capf, sm, pol, [&](uint64_t rc, uint32_t p) {
+      uint32_t f = 0;  // the fine bin of sorted position p
+      while (f + 1 < pl.F2 && sm.hist[f + 1] <= p) ++f;
+      const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
+      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
+    });
+    __syncthreads();
+  }
+  block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
+}
+
+// ---------------------------------------------------------------------------
+// probe: one persistent CTA per SM, fine regions resident in shared memory
+// ---------------------------------------------------------------------------
+
+constexpr int kPWarps = 16;                     // consumer warps
+constexpr int kPConsumers = kPWarps * 32;
+constexpr int kPThreads = kPConsumers + 32;     // + one producer warp
+constexpr int kPChunk = 4096;                   // records per ring stage
+constexpr int kPStages = 3;
+constexpr int kPPerLane = kPChunk / kPConsumers;  // records per consumer lane per chunk
+template <int WPB>
+constexpr int kPSub = (16 / WPB) < kPPerLane ? (16 / WPB) : kPPerLane;  // records in flight per lane
+constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + 128;
+
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPConsumers) : "memory"); }
+
+// Queue unplaced inserts for the eviction pass: one reservation per warp for
+// the whole sub-batch, then the keys are re-read (scattered, ~4 % of keys)
+// and hashed.  Whole warp, converged.
+template <int K>
+__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K],
+                                                    const Geo& g) {
+  const int lane = threadIdx.x & 31;
+  const uint32_t c = __popc(nm);
+  uint32_t incl = c;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+    if (lane >= d) incl += y;
+  }
+  const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+  if (!total) return;
+  unsigned long long base = 0;
+  if (lane == 31) base = atomicAdd(&sk.ctr->n_queued, (unsigned long long)total);
+  base = __shfl_sync(0xffffffffu, base, 31);
+  uint64_t pos = base + incl - c;
+  uint64_t k[K];
+#pragma unroll
+  for (int q = 0; q < K; ++q) k[q] = ((nm >> q) & 1u) ? sk.keys[rc[q] >> 32] : 0;
+#pragma unroll
+  for (int q = 0; q < K; ++q) {
+    if (!((nm >> q) & 1u)) continue;
+    const uint32_t idx = (uint32_t)(rc[q] >> 32);
+    if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, sk.hashed ? k[q] : xxh64(k[q], g.seed), 0u, 0u};
+    else if (sk.ok) sk.ok[idx] = 0;
+    ++pos;
+  }
+}
+
+// PHASE 1: records of the primary bucket; misses are appended to this CTA's
+// dense miss segment (re-binned by their alternate bucket for phase 2).
+// PHASE 2: records of the alternate bucket; inserts still unplaced are queued
+// for the eviction pass.
+//
+// Warp roles: warp kPWarps is the producer -- one lane streams this CTA's
+// record chunks (its regions in turn, each region's chunks in turn) into a
+// kPStages-deep ring with cp.async.bulk, gated by per-stage full/empty
+// mbarriers.  Warps 0..kPWarps-1 consume: each owns a fixed slice of every
+// chunk, so they never wait for each other except at region boundaries, where
+// consumer thread 0 writes the table slice back and loads the next one.
+template <int OP, int F, int WPB, int POL, int PHASE>
+__global__ void __launch_bounds__(kPThreads, 1)
+    region_probe_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
+  extern __shared__ __align__(128) uint8_t dsm[];
+  uint64_t* tab = reinterpret_cast<uint64_t*>(dsm);
+  uint64_t* ring = reinterpret_cast<uint64_t*>(dsm + kRegionSmem);
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8);
+  uint64_t* empty = full + kPStages;
+  uint64_t* tbar = empty + kPStages;
+  __shared__ uint32_t s_miss[1];
+  constexpr bool kMut = OP != OP_QUERY;
+  const uint32_t* cnt = w.cntf;
+  const uint64_t* bins = w.binf;
+  const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+  const uint32_t rb = 1u << pl.lrb;
+  constexpr uint32_t bbytes = WPB * 8;
+  if (tid == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(full + s, 1);
+      mbar_init(empty + s, kPWarps);
+    }
+    mbar_init(tbar, 1);
+    fence_mbar_init();
+    s_miss[0] = 0;
+  }
+  __syncthreads();
+
+  auto region_count = [&](uint32_t r) -> uint32_t {
+    const uint32_t c = cnt[(size_t)r * kCntStride];
+    return c < pl.capf ? c : (uint32_t)pl.capf;
+  };
+  auto region_buckets = [&](uint32_t r) -> uint32_t {
+    const uint64_t b0 = (uint64_t)r << pl.lrb;
+    return (uint32_t)(g.m > b0 ? min((uint64_t)rb, g.m - b0) : 0);
+  };
+  uint32_t n_ok = 0, n_alt = 0;
+
+  if (warp == kPWarps) {
+    // ---- producer ----
+    if (lane == 0) {
+      uint32_t iseq = 0;
+      for (uint32_t r = blockIdx.x; r < pl.R; r += gridDim.x) {
+        const uint32_t cn = region_count(r);
+        for (uint32_t k0 = 0; k0 < cn; k0 += kPChunk, ++iseq) {
+          const uint32_t s = iseq % kPStages;
+          if (iseq >= (uint32_t)kPStages) mbar_wait(empty + s, ((iseq / kPStages) - 1u) & 1u);
+          const uint32_t len = min((uint32_t)kPChunk, cn - k0);
+          const uint32_t bytes = ((len + 1u) & ~1u) * 8u;  // bins are even-sized and 16 B aligned
+          mbar_expect_tx(full + s, bytes);
+          bulk_g2s(ring + (size_t)s * kPChunk, bins + (uint64_t)r * pl.capf + k0, bytes, full + s);
+        }
+      }
+    }
+  } else {
+    // ---- consumers ----
+    const uint64_t fpmask = (1ull << pl.pb) - 1u;
+    const uint32_t tab_a = saddr(tab);
+    const uint64_t pol = evict_first_policy();
+    auto next_region = [&](uint32_t r) -> uint32_t {  // next region of this CTA with records
+      while (r < pl.R && region_count(r) == 0) r += gridDim.x;
+      return r;
+    };
+    auto load_table = [&](uint32_t r) {  // consumer thread 0
+      const uint32_t nb = region_buckets(r);
+      mbar_expect_tx(tbar, nb * bbytes);
+      bulk_g2s(tab, words + ((uint64_t)r << pl.lrb) * WPB, nb * bbytes, tbar);
+      const uint32_t rn = next_region(r + gridDim.x);
+      if (rn < pl.R) prefetch_l2(words + ((uint64_t)rn << pl.lrb) * WPB, region_buckets(rn) * bbytes);
+    };
+    uint32_t r = next_region(blockIdx.x);
+    if (tid == 0 && r < pl.R) load_table(r);
+    uint32_t cseq = 0, tpar = 0;
+    for (; r < pl.R;) {
+      const uint32_t cn = region_count(r);
+      const uint64_t b0 = (uint64_t)r << pl.lrb;
+      mbar_wait(tbar, tpar);
+      tpar ^= 1u;
+      for (uint32_t k0 = 0; k0 < cn; k0 += kPChunk, ++cseq) {
+        const uint32_t s = cseq % kPStages;
+        mbar_wait(full + s, (cseq / kPStages) & 1u);
+        const uint32_t len = min((uint32_t)kPChunk, cn - k0);
+        const uint64_t* rs = ring + (size_t)s * kPChunk + warp * (kPPerLane * 32) + lane;
+        const uint32_t kbase = warp * (kPPerLane * 32) + lane;
+#pragma unroll 1
+        for (int q0 = 0; q0 < kPPerLane; q0 += kPSub<WPB>) {
+          constexpr int K = kPSub<WPB>;
+          uint64_t rc[K];
+          uint64_t wv[K][WPB];
+          uint32_t vm = 0;  // bit q: record q valid
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            const bool v = kbase + (q0 + q) * 32 < len;
+            vm |= (uint32_t)v << q;
+            rc[q] = v ? rs[(q0 + q) * 32] : 0;
+            const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
+            // queries snapshot all buckets up front; mutations snapshot right
+            // before their CAS (a stale snapshot costs a whole-warp retry)
+            if (OP == OP_QUERY && v) lds_bucket<WPB>(tab_a + loc * bbytes, wv[q]);
+          }
+          uint32_t nm = 0;  // bit q: record q not resolved here
+          uint64_t i2[K];
+#pragma unroll
+          for (int q = 0; q < K; ++q) {
+            if (!((vm >> q) & 1u)) continue;
+            const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
+            const uint64_t fp = rc[q] & fpmask;
+            const uint32_t idx = (uint32_t)(rc[q] >> 32);
+            if constexpr (OP == OP_QUERY) {
+              const bool hit = match_any<F, WPB, POL>(wv[q], fp);
+              if (hit) set_bit(sk.bits, idx);
+              if (PHASE == 1 && !hit) {
+                nm |= 1u << q;
+                uint64_t cc;
+                i2[q] = alt_index<POL>(b0 + loc, fp, 0, g, cc);
+              }
+            } else {
+              const uint32_t a = tab_a + loc * bbytes;
+              const uint64_t tag = PHASE == 1 ? fp : (POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp);
+              lds_bucket<WPB>(a, wv[q]);
+              const bool done =
+                  OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv[q]) : smem_remove<F, WPB>(a, tag, wv[q]);
+              n_ok += done;
+              if (OP == OP_DELETE && done) set_bit(sk.bits, idx);
+              if (!done) {
+                nm |= 1u << q;
+                if constexpr (PHASE == 1) {
+                  uint64_t cc;
+                  i2[q] = alt_index<POL>(b0 + loc, fp, 0, g, cc);
+                }
+              }
+            }
+          }
+          if constexpr (PHASE == 1) {
+            // misses go to this CTA's dense segment (warp reservation on a
+            // shared-memory counter), re-binned by alternate bucket for phase 2
+            const uint32_t c = __popc(nm);
+            n_alt += c;
+            uint32_t incl = c;
+#pragma unroll
+            for (int d = 1; d < 32; d <<= 1) {
+              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+              if (lane >= d) incl += y;
+            }
+            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+            if (total) {
+              uint32_t base = 0;
+              if (lane == 31) base = atomicAdd(s_miss, total);
+              base = __shfl_sync(0xffffffffu, base, 31);
+              uint4* dst = w.miss + (uint64_t)blockIdx.x * w.seg + base + incl - c;
+#pragma unroll
+              for (int q = 0; q < K; ++q)
+                if ((nm >> q) & 1u)
+                  *dst++ = make_uint4((uint32_t)(rc[q] >> 32), (uint32_t)(rc[q] & fpmask), (uint32_t)i2[q],
+                                      (uint32_t)(i2[q] >> 32));
+            }
+          } else if constexpr (OP == OP_INSERT && PHASE == 2) {
+            enqueue_evict_batch<K>(sk, nm, rc, g);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(empty + s);  // this warp is done with stage s
+      }
+      // region boundary: write the slice back, bring in the next one
+      if (kMut) fence_async_smem();  // this thread's shared-memory CASes before the bulk copy
+      consumers_sync();
+      const uint32_t rn = next_region(r + gridDim.x);
+      if (tid == 0) {
+        if (kMut) {
+          bulk_s2g(words + b0 * WPB, tab, region_buckets(r) * bbytes);
+          bulk_wait_read();  // the slice has left shared memory
+        }
+        if (rn < pl.R) load_table(rn);
+      }
+      r = rn;
+    }
+    if (tid == 0) bulk_wait_all();
+  }
+  block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);  // (synchronizes the block)
+  if (PHASE == 1 && tid == 0) w.n_miss[blockIdx.x] = s_miss[0];
+}
+
+// bitmap -> one byte per key, and (queries) the hit count
+__global__ void __launch_bounds__(256) expand_count_kernel(const uint32_t* __restrict__ bits, uint64_t n,
+                                                           uint8_t* __restrict__ out, ckf_counters* ctr) {
+  const uint64_t nw = (n + 31) / 32;
+  uint32_t hits = 0;
+  for (uint64_t wi = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; wi < nw; wi += (uint64_t)gridDim.x * blockDim.x) {
+    uint32_t b = bits[wi];
+    const uint64_t i0 = wi * 32;
+    if (i0 + 32 > n) b &= (1u << (n - i0)) - 1u;
+    hits += __popc(b);
+    if (i0 + 32 <= n && ((uintptr_t)(out + i0) & 15) == 0) {
+      uint32_t q[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t nib = (b >> (4 * k)) & 0xF;
+        q[k] = (nib & 1) | ((nib >> 1 & 1) << 8) | ((nib >> 2 & 1) << 16) | ((nib >> 3 & 1) << 24);
+      }
+      reinterpret_cast<uint4*>(out + i0)[0] = make_uint4(q[0], q[1], q[2], q[3]);
+      reinterpret_cast<uint4*>(out + i0)[1] = make_uint4(q[4], q[5], q[6], q[7]);
+    } else {
+      for (uint64_t i = i0; i < n && i < i0 + 32; ++i) out[i] = (b >> (i - i0)) & 1u;
+    }
+  }
+  if (ctr) block_count_add(hits, 0, ctr, nullptr, +1);
+}
+
+}  // namespace ckf
