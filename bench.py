@@ -300,14 +300,20 @@ def run_ours(args) -> None:
         op_stats[o] = {"G_ops_s": round(gops, 3), "ms": round(per_op[o] / args.steps, 4),
                        "bytes_per_op": round(bpo, 2), "p2": round(p2[o], 4),
                        "achieved_GBs": round(gops * bpo, 1), "frac": round(gops * bpo / peaks["hbm_gbs"], 4)}
+    # The dominant op is a fixed pipeline of kernels on one stream (region schedule:
+    # bin -> split -> probe on i1, bin -> split -> probe on i2, + evict / bit expansion);
+    # its CUDA-event time above is the launch duration the roofline is taken over.
     dom = max(ops, key=lambda o: per_op[o])
-    traffic = None
+    traffic, kernels = None, None
     tf = ROOT / "profiles" / "traffic.json"
     if tf.exists():
-        traffic = json.loads(tf.read_text()).get(dom)
+        tj = json.loads(tf.read_text())
+        traffic = tj.get(dom)
+        kernels = [k[0] for k in tj.get(dom + "_kernels", [])]
     roofline = {"bound": "hbm", "achieved": op_stats[dom]["achieved_GBs"], "peak": peaks["hbm_gbs"],
                 "unit": "GB/s", "frac": op_stats[dom]["frac"], "traffic": traffic,
-                "kernel": f"{dom} ({'insert_kernel+evict_kernel' if dom == 'insert' else dom.rstrip('+-') + '_kernel'})",
+                "kernel": f"{dom} ({'+'.join(kernels) if kernels else 'op pipeline'})",
+                "traffic_source": "profiles/traffic.json (ncu dram__bytes_read+write summed over the op's kernels)",
                 "peak_source": peaks["source"],
                 "random_sector_ceiling": "~48 G random 32B sectors/s at 512 MiB (profiles/r01_probe_ceiling.txt)"}
 

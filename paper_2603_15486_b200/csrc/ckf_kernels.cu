@@ -166,7 +166,7 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
       }
       need = !done;
       n_ok += done;
-      ok[i] = done ? 1 : 0;
+      ok[i] = 1;  // a queued key stays 1 unless the eviction pass fails it
       if (ev) ev[i] = 0;
       if (lost) lost[i] = 0;
     }
@@ -210,7 +210,7 @@ __global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restri
     Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
     rec[r] = ckf_record{i, o.lost, o.rounds, o.ok};
     n_ok += o.ok;
-    ok[i] = (uint8_t)o.ok;
+    if (!o.ok) ok[i] = 0;  // queued keys enter with ok = 1 (scattered byte writes only on failure)
     if (ev) ev[i] = o.rounds;
     if (lost) lost[i] = o.lost;
   }
@@ -521,7 +521,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   uint32_t lrbc = lm > 9 ? lm - 9 : 0;
   if (lrbc < lrb) lrbc = lrb;
   if (lrbc + pb > 31) lrbc = 31 - pb;
-  if (lrbc - lrb > 6) lrbc = lrb + 6;  // F2 <= 64
+  if (lrbc - lrb > 3) lrbc = lrb + 3;  // F2 <= 8
   const uint64_t R1 = (m + (1ull << lrbc) - 1) >> lrbc;
   if (R1 > (uint64_t)kRMaxCoarse) return pl;
   pl.lrb = lrb;
@@ -604,8 +604,8 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
                       cudaStream_t s) {
   RWork w = rwork_view(ws, L, pl);
   if (cudaMemsetAsync(ws, 0, L.ctr_end, s) != cudaSuccess) return cuda_error();  // bin + miss counters
-  if (OP != OP_INSERT) {
-    if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
+  if (OP != OP_INSERT) {  // all-true: only final negatives clear their bit
+    if (cudaMemsetAsync(w.bits, 0xFF, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
     sk.bits = w.bits;
   }
   sk.keys = keys;

@@ -27,6 +27,8 @@
 // the only copy being mutated.
 #pragma once
 
+#include <type_traits>
+
 #include "ckf_tiled.cuh"
 
 namespace ckf {
@@ -135,28 +137,37 @@ __device__ __forceinline__ bool match_any(const uint64_t (&w)[WPB], uint64_t fp)
 }
 
 // kB-bit mask over the bucket's slots (slot = word * tpw + lane) of lanes equal
-// to `pat` (pat = 0: empty lanes)
+// to `pat` (pat = 0: empty lanes); 32-bit when the bucket has <= 32 slots
 template <int F, int WPB>
-__device__ __forceinline__ uint64_t slot_mask(const uint64_t (&w)[WPB], uint64_t pat) {
+using SlotMask = typename std::conditional<(WPB * 64 / F <= 32), uint32_t, uint64_t>::type;
+
+template <int F, int WPB>
+__device__ __forceinline__ SlotMask<F, WPB> slot_mask(const uint64_t (&w)[WPB], uint64_t pat) {
   constexpr int kTpw = 64 / F;
-  uint64_t m = 0;
+  SlotMask<F, WPB> m = 0;
 #pragma unroll
-  for (int j = 0; j < WPB; ++j) m |= (uint64_t)lane_mask<F>(w[j] ^ pat) << (j * kTpw);
+  for (int j = 0; j < WPB; ++j) m |= (SlotMask<F, WPB>)lane_mask<F>(w[j] ^ pat) << (j * kTpw);
   return m;
 }
 
 // First slot of `m` in the reference scan order: words from `start` wrapping,
 // lowest lane first (K:166-179, K:207-220).  -1 if none.
 template <int F, int WPB>
-__device__ __forceinline__ int first_slot(uint64_t m, int start) {
+__device__ __forceinline__ int first_slot(SlotMask<F, WPB> m, int start) {
   constexpr int kTpw = 64 / F, kB = WPB * kTpw;
   const int sh = start * kTpw;
-  uint64_t rot;
-  if constexpr (kB == 64) rot = sh ? (m >> sh) | (m << (64 - sh)) : m;
-  else rot = ((m >> sh) | (m << (kB - sh))) & ((1ull << kB) - 1u);
-  if (!rot) return -1;
-  const int f = __ffsll((long long)rot) - 1 + sh;
-  return f >= kB ? f - kB : f;
+  if constexpr (kB <= 32) {
+    const uint32_t full = kB == 32 ? ~0u : ((1u << kB) - 1u);
+    const uint32_t rot = kB == 32 ? __funnelshift_r(m, m, sh) : (((m >> sh) | (m << ((kB - sh) & 31))) & full);
+    if (!rot) return -1;
+    const int f = __ffs((int)rot) - 1 + sh;
+    return f >= kB ? f - kB : f;
+  } else {
+    const uint64_t rot = sh ? (m >> sh) | (m << (64 - sh)) : m;
+    if (!rot) return -1;
+    const int f = __ffsll((long long)rot) - 1 + sh;
+    return f >= kB ? f - kB : f;
+  }
 }
 
 template <int WPB>
@@ -168,19 +179,34 @@ __device__ __forceinline__ uint64_t pick(const uint64_t (&w)[WPB], int j) {
   return r;
 }
 
+// Lost CAS: the word we lost on now holds `old`; refresh only that word's
+// lanes in the slot mask (a retry costs ~15 instructions instead of a rescan;
+// under SIMT the whole warp pays for any lane's retry).
+template <int F, int WPB>
+__device__ __forceinline__ void refresh_word(SlotMask<F, WPB>& m, uint64_t (&w)[WPB], int j, uint64_t old,
+                                             uint64_t pat) {
+  constexpr int kTpw = 64 / F;
+  constexpr SlotMask<F, WPB> kLanes = (SlotMask<F, WPB>)((1ull << kTpw) - 1u);
+#pragma unroll
+  for (int q = 0; q < WPB; ++q)
+    if (j == q) w[q] = old;
+  m = (m & ~(kLanes << (j * kTpw))) | ((SlotMask<F, WPB>)lane_mask<F>(old ^ pat) << (j * kTpw));
+}
+
 // TryInsert on a shared-memory bucket (a = its shared address, w = snapshot).
-// A lost CAS reloads the bucket and decides again.
 template <int F, int WPB>
 __device__ __forceinline__ bool smem_insert(uint32_t a, uint64_t tag, uint64_t (&w)[WPB]) {
   constexpr int kTpw = 64 / F, kB = WPB * kTpw;
   const int start = (int)(tag % kB) / kTpw;
+  SlotMask<F, WPB> m = slot_mask<F, WPB>(w, 0);
   while (true) {
-    const int slot = first_slot<F, WPB>(slot_mask<F, WPB>(w, 0), start);
+    const int slot = first_slot<F, WPB>(m, start);
     if (slot < 0) return false;
     const int j = slot / kTpw, lane = slot % kTpw;
     const uint64_t bw = pick<WPB>(w, j);
-    if (cas_shared(a + 8u * j, bw, bw | (tag << (lane * F))) == bw) return true;
-    lds_bucket<WPB>(a, w);
+    const uint64_t old = cas_shared(a + 8u * j, bw, bw | (tag << (lane * F)));
+    if (old == bw) return true;
+    refresh_word<F, WPB>(m, w, j, old, 0);
   }
 }
 
@@ -190,15 +216,21 @@ __device__ __forceinline__ bool smem_remove(uint32_t a, uint64_t tag, uint64_t (
   constexpr int kTpw = 64 / F, kB = WPB * kTpw;
   const int start = (int)(tag % kB) / kTpw;
   const uint64_t pat = Lanes<F>::bcast(tag);
+  SlotMask<F, WPB> m = slot_mask<F, WPB>(w, pat);
   while (true) {
-    const int slot = first_slot<F, WPB>(slot_mask<F, WPB>(w, pat), start);
+    const int slot = first_slot<F, WPB>(m, start);
     if (slot < 0) return false;
     const int j = slot / kTpw, lane = slot % kTpw;
     const uint64_t bw = pick<WPB>(w, j);
-    if (cas_shared(a + 8u * j, bw, bw & ~(Lanes<F>::kLaneMask << (lane * F))) == bw) return true;
-    lds_bucket<WPB>(a, w);
+    const uint64_t old = cas_shared(a + 8u * j, bw, bw & ~(Lanes<F>::kLaneMask << (lane * F)));
+    if (old == bw) return true;
+    refresh_word<F, WPB>(m, w, j, old, pat);
   }
 }
+
+// Region-schedule results start all-true; only keys that end up negative /
+// not deleted cost a (random, L2-resident) bitmap update.
+__device__ __forceinline__ void clear_bit(uint32_t* bits, uint32_t i) { atomicAnd(bits + (i >> 5), ~(1u << (i & 31))); }
 
 // ---------------------------------------------------------------------------
 // plan, records, workspace
@@ -258,8 +290,9 @@ __device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, ui
   }
   if (done) {
     if (OP != OP_QUERY) ++n_ok;
-    if (OP != OP_INSERT) set_bit(sk.bits, idx);
-  } else if (OP == OP_INSERT) {
+  } else if (OP != OP_INSERT) {
+    clear_bit(sk.bits, idx);  // results start all-true (region schedule)
+  } else {
     const uint64_t k = sk.keys[idx];
     enqueue_evict_one(sk, idx, sk.hashed ? k : xxh64(k, g.seed));
   }
@@ -371,7 +404,6 @@ __global__ void __launch_bounds__(kBThreads, 3)
       const uint64_t nx = t0 + (uint64_t)gridDim.x * KT;
       if (nx < n && n - nx >= 2) {
         if (SRC == SRC_KEYS) prefetch_l2(keys + nx, (uint32_t)(min((uint64_t)KT, n - nx) * 8) & ~15u);
-        else prefetch_l2(ms + nx, (uint32_t)min((uint64_t)KT, n - nx) * 16);
       }
     }
     for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.hist[r] = 0;
@@ -515,14 +547,14 @@ __global__ void __launch_bounds__(kBThreads, 3)
 // probe: one persistent CTA per SM, fine regions resident in shared memory
 // ---------------------------------------------------------------------------
 
-constexpr int kPWarps = 16;                     // consumer warps
+constexpr int kPWarps = 30;                     // consumer warps
 constexpr int kPConsumers = kPWarps * 32;
-constexpr int kPThreads = kPConsumers + 32;     // + one producer warp
-constexpr int kPChunk = 4096;                   // records per ring stage
+constexpr int kPThreads = kPConsumers + 32;     // + one producer warp (<= 1024 threads)
+constexpr int kPPerLane = 4;                    // records per consumer lane per chunk
+constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (3840)
 constexpr int kPStages = 3;
-constexpr int kPPerLane = kPChunk / kPConsumers;  // records per consumer lane per chunk
 template <int WPB>
-constexpr int kPSub = (16 / WPB) < kPPerLane ? (16 / WPB) : kPPerLane;  // records in flight per lane
+constexpr int kPSub = (8 / WPB) < kPPerLane ? (8 / WPB) : kPPerLane;  // records in flight per lane
 constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + 128;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
@@ -683,7 +715,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint32_t idx = (uint32_t)(rc[q] >> 32);
             if constexpr (OP == OP_QUERY) {
               const bool hit = match_any<F, WPB, POL>(wv[q], fp);
-              if (hit) set_bit(sk.bits, idx);
+              if (PHASE == 2 && !hit) clear_bit(sk.bits, idx);  // a final negative
               if (PHASE == 1 && !hit) {
                 nm |= 1u << q;
                 uint64_t cc;
@@ -696,7 +728,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
               const bool done =
                   OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv[q]) : smem_remove<F, WPB>(a, tag, wv[q]);
               n_ok += done;
-              if (OP == OP_DELETE && done) set_bit(sk.bits, idx);
+              if (OP == OP_DELETE && PHASE == 2 && !done) clear_bit(sk.bits, idx);  // tag in neither bucket
               if (!done) {
                 nm |= 1u << q;
                 if constexpr (PHASE == 1) {

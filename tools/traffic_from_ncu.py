@@ -22,8 +22,13 @@ ours = [d for d in seq if "ckf::" in d["name"]]
 for d in ours:
     m = re.search(r"ckf::(\w+)<([^>]*)>", d["name"]) or re.search(r"ckf::(\w+)", d["name"])
     d["short"] = m.group(1)
-    d["op"] = int(m.group(2).split(",")[0]) if m.lastindex and m.lastindex > 1 and m.group(1).startswith("tile") else None
-# walk backwards: the last delete, lookup-, lookup+, insert of the timed step
+    args = [a.strip() for a in m.group(2).split(",")] if m.lastindex and m.lastindex > 1 else []
+    d["op"] = int(args[0]) if args and m.group(1).startswith(("tile", "region")) else None
+    # a new op call starts at its first pass: the keys' bin kernel (region SRC_KEYS = 0) or a direct kernel
+    d["start"] = (d["short"] == "tile_bin_kernel" or (d["short"] == "region_bin_kernel" and args[-1] == "0")
+                  or d["short"] in ("insert_kernel", "query_kernel", "delete_kernel"))
+
+
 def op_of(d):
     if d["short"] in ("insert_kernel", "evict_kernel"):
         return "insert"
@@ -34,14 +39,12 @@ def op_of(d):
     if d["op"] is not None:
         return {0: "query", 1: "insert", 2: "delete"}[d["op"]]
     return None
+
+
 groups = []
 for d in ours:
     o = op_of(d)
-    if o is None:
-        if groups:
-            groups[-1][1].append(d)
-        continue
-    if not groups or groups[-1][0] != o or (o == "query" and d["short"] in ("tile_bin_kernel", "query_kernel")):
+    if d["start"] or not groups:
         groups.append((o, [d]))
     else:
         groups[-1][1].append(d)
