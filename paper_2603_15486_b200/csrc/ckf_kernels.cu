@@ -495,6 +495,8 @@ static uint32_t ceil_log2(uint64_t x) {
   return l;
 }
 
+constexpr uint32_t kMaxProbeGrid = 1024;
+
 static uint64_t even_cap(double per) { return ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + 1) & ~1ull; }
 
 // Region plan; ok=false when the schedule does not apply to this table.
@@ -532,13 +534,15 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   pl.pb = pb;
   const double recs = (double)n;
   (void)op;
-  pl.cap1 = even_cap(recs / pl.R1);
-  pl.capf = even_cap(recs / pl.R);
+  // + run padding: at most one filler per bin per tile of the pass that fills it
+  // (bin: ceil(n / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
+  const uint64_t tiles1 = (n + kBTile - 1) / kBTile + (uint64_t)kMaxProbeGrid;
+  pl.cap1 = (even_cap(recs / pl.R1) + tiles1 + 1) & ~1ull;
+  pl.capf = (even_cap(recs / pl.R) + (pl.cap1 + kBTile - 1) / kBTile + 1) & ~1ull;
   ok = true;
   return pl;
 }
 
-constexpr uint32_t kMaxProbeGrid = 1024;
 
 // one persistent probe CTA per SM (fewer if there are fewer regions)
 static uint32_t probe_grid(const RPlan& pl) {

@@ -306,17 +306,24 @@ __device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, ui
 constexpr int kBThreads = 256;
 constexpr int kBItems = 16;
 constexpr int kBTile = kBThreads * kBItems;  // records per tile
-constexpr uint32_t kNoSlot = 0xFFFFFFFFu;    // the record's bin is full
+// Runs go out as TMA bulk copies, which need 16 B granules: a run of odd
+// length is padded with one filler record (index 0xFFFFFFFF, never a key:
+// batches hold < 2^32 - 1 keys) that every consumer skips.
+constexpr uint64_t kFiller = ~0ull;
+__device__ __forceinline__ bool is_filler(uint64_t rc) { return (uint32_t)(rc >> 32) == 0xFFFFFFFFu; }
 
 struct BinSmem {
-  uint64_t rec[kBTile];
-  uint32_t dst[kBTile];   // destination slot (bin * cap + offset), or kNoSlot
-  uint32_t hist[kRMaxCoarse];  // counts, then exclusive starts
-  uint32_t off[kRMaxCoarse];   // global run base - start (mod 2^32)
+  uint64_t rec[kBTile + kRMaxCoarse];  // sorted tile (bulk writer: runs padded to even length)
+  uint32_t dst[kBTile];                // coalesced writer: destination slot of each sorted record
+  uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
+  uint32_t start[kRMaxCoarse];         // run start in rec (even)
+  uint32_t gbase[kRMaxCoarse];         // run start in the bin (even)
   uint32_t warp_sums[kBThreads / 32];
 };
 
-// counts in sm.hist -> exclusive starts in sm.hist, global bases - start in sm.off
+// sm.cnt (records per bin) -> sm.start (exclusive scan of the padded run
+// lengths) and sm.gbase (one global reservation per non-empty bin)
+template <bool kBulk>
 __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem& sm) {
   constexpr int NW = kBThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
@@ -326,7 +333,7 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const uint32_t r = lo + k;
-    c[k] = r < hi ? sm.hist[r] : 0u;
+    c[k] = r < hi ? (kBulk ? (sm.cnt[r] + 1u) & ~1u : sm.cnt[r]) : 0u;
     gb[k] = c[k] ? atomicAdd(gcnt + (size_t)r * kCntStride, c[k]) : 0u;
     sum += c[k];
   }
@@ -353,34 +360,84 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
   for (int k = 0; k < 2; ++k) {
     const uint32_t r = lo + k;
     if (r < hi) {
-      sm.hist[r] = run;
-      sm.off[r] = gb[k] - run;
+      sm.start[r] = run;
+      sm.gbase[r] = gb[k];
+      if (kBulk && (sm.cnt[r] & 1u)) sm.rec[run + sm.cnt[r]] = kFiller;
       run += c[k];
     }
   }
 }
 
-// Places record `rc` of bin b at its sorted tile position p, with its
-// destination slot (bins are laid out bin * cap + offset; < 2^32 slots).
+template <bool kBulk>
 __device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc, uint64_t cap) {
-  const uint32_t p = sm.hist[b] + rank;
-  const uint32_t o = sm.off[b] + p;  // offset inside the bin
+  const uint32_t p = sm.start[b] + rank;
   sm.rec[p] = rc;
-  sm.dst[p] = o < cap ? b * (uint32_t)cap + o : kNoSlot;
+  if (!kBulk) {  // slot in the bin array (bin * cap + offset < 2^32), or none: bin full
+    const uint32_t o = sm.gbase[b] + rank;
+    sm.dst[p] = o < cap ? b * (uint32_t)cap + o : 0xFFFFFFFFu;
+  }
 }
 
-// Writes the tile's sorted records (`total` of them) to their slots; records
-// whose bin is full go to ovf(rec, p).
+// Coalesced writer (short runs): thread p stores sorted record p.  Caller: all
+// threads, after bin_place<false>; records of full bins go to ovf(rec, bin).
 template <class Ovf>
-__device__ __forceinline__ void bin_write(uint32_t total, uint64_t* __restrict__ out, BinSmem& sm, uint64_t pol,
-                                          Ovf&& ovf) {
+__device__ __forceinline__ void bin_write_coalesced(uint32_t nb, uint32_t total, uint64_t* __restrict__ out,
+                                                    uint64_t cap, BinSmem& sm, uint64_t pol, Ovf&& ovf) {
+  __syncthreads();
   for (uint32_t p = threadIdx.x; p < total; p += kBThreads) {
     const uint32_t d = sm.dst[p];
     const uint64_t rc = sm.rec[p];
-    if (d != kNoSlot) st_stream_ef(out + d, rc, pol);
-    else ovf(rc, p);
+    if (d != 0xFFFFFFFFu) {
+      st_stream_ef(out + d, rc, pol);
+    } else {
+      // the bin of sorted position p: the last bin starting at or before p
+      // (empty bins share the start of the next one)
+      uint32_t lo = 0, hi = nb - 1;
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi + 1) >> 1;
+        if (sm.start[mid] <= p) lo = mid;
+        else hi = mid - 1;
+      }
+      ovf(rc, lo);
+    }
   }
 }
+
+// Sends every (tile, bin) run to its bin with one bulk copy.  A run that does
+// not fit its bin (adversarial inputs only) goes record by record: the part
+// that fits by plain stores, the rest to ovf(rec, bin).  Caller: all threads,
+// after bin_place; shared memory is released by bin_release().
+template <class Ovf>
+__device__ __forceinline__ void bin_write(uint32_t nb, uint64_t* __restrict__ out, uint64_t cap, BinSmem& sm,
+                                          Ovf&& ovf) {
+  fence_async_smem();  // this thread's placements -> visible to the bulk copies
+  __syncthreads();
+  bool issued = false;
+  for (uint32_t r = threadIdx.x; r < nb; r += kBThreads) {
+    const uint32_t c = sm.cnt[r];
+    if (!c) continue;
+    const uint32_t cr = (c + 1u) & ~1u, st = sm.start[r], gb = sm.gbase[r];
+    uint64_t* dst = out + (uint64_t)r * cap;
+    if ((uint64_t)gb + cr <= cap) {
+      asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + gb),
+                   "r"(saddr(&sm.rec[st])), "r"(cr * 8u)
+                   : "memory");
+      issued = true;
+    } else {
+      for (uint32_t k = 0; k < c; ++k) {
+        const uint64_t rc = sm.rec[st + k];
+        if ((uint64_t)gb + k < cap) dst[gb + k] = rc;
+        else ovf(rc, r);
+      }
+      if ((c & 1u) && (uint64_t)gb + c < cap) dst[gb + c] = kFiller;
+    }
+  }
+  if (issued) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+}
+
+// Before the tile's shared memory is rewritten: this thread's bulk copies have
+// read it (the caller synchronizes the block afterwards).
+__device__ __forceinline__ void bin_release() { bulk_wait_read(); }
 
 // SRC_KEYS: the batch's keys (or hashes), one record per key for its primary
 // bucket.  SRC_MISS: phase-1 misses {idx, fp, i2} from probe-CTA segment
@@ -406,7 +463,8 @@ __global__ void __launch_bounds__(kBThreads, 3)
         if (SRC == SRC_KEYS) prefetch_l2(keys + nx, (uint32_t)(min((uint64_t)KT, n - nx) * 8) & ~15u);
       }
     }
-    for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.hist[r] = 0;
+    bin_release();
+    for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.cnt[r] = 0;
     uint64_t rec[kBItems];
     uint32_t pk[kBItems];  // bin << 16 | rank; 0xFFFFFFFF = no record
     if constexpr (SRC == SRC_KEYS) {
@@ -433,7 +491,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
         const uint64_t i1 = reduce_index(h & 0xFFFFFFFFull, g);
         const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
         rec[q] = rpack(i, 0u, i1 & lmask, fp, pl.pb);
-        pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.hist[b1], 1u) : 0xFFFFFFFFu;
+        pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
       }
     } else {
       __syncthreads();  // hist zeroed
@@ -451,31 +509,26 @@ __global__ void __launch_bounds__(kBThreads, 3)
           const uint64_t i2 = (uint64_t)e[q].z | ((uint64_t)e[q].w << 32);
           const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
           rec[q0 + q] = rpack(e[q].x, 1u, i2 & lmask, e[q].y, pl.pb);
-          pk[q0 + q] = i < n ? (b2 << 16) | atomicAdd(&sm.hist[b2], 1u) : 0xFFFFFFFFu;
+          pk[q0 + q] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
       }
     }
     __syncthreads();
-    bin_reserve(pl.R1, w.cnt1, sm);
+    constexpr bool kBulk = SRC == SRC_MISS;  // (measured: keys bin faster with coalesced stores)
+    bin_reserve<kBulk>(pl.R1, w.cnt1, sm);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
-      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
-    __syncthreads();
-    const uint32_t total = (uint32_t)min((uint64_t)KT, n - t0);
-    bin_write(total, w.bin1, sm, pol, [&](uint64_t rc, uint32_t p) {
-      // the bin of sorted position p: the last bin whose start is <= p
-      uint32_t lo = 0, hi = pl.R1 - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (sm.hist[mid] <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      const uint64_t bucket = ((uint64_t)lo << pl.lrbc) + ((rc >> pl.pb) & lmask);
+      if (pk[q] != 0xFFFFFFFFu) bin_place<kBulk>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
+    auto ovf = [&](uint64_t rc, uint32_t b) {
+      const uint64_t bucket = ((uint64_t)b << pl.lrbc) + ((rc >> pl.pb) & lmask);
       resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
-    });
+    };
+    if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
+    else bin_write_coalesced(pl.R1, (uint32_t)min((uint64_t)KT, n - t0), w.bin1, pl.cap1, sm, pol, ovf);
     __syncthreads();
   }
+  bulk_wait_all();
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
@@ -501,7 +554,8 @@ __global__ void __launch_bounds__(kBThreads, 3)
     const uint32_t cc = w.cnt1[(size_t)c * kCntStride];
     const uint64_t cnt = cc < pl.cap1 ? cc : pl.cap1;
     if (off0 >= cnt) continue;  // block-uniform
-    for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.hist[r] = 0;
+    bin_release();
+    for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.cnt[r] = 0;
     const uint64_t* src = w.bin1 + c * pl.cap1 + off0;
     const uint32_t nrec = (uint32_t)min((uint64_t)kBTile, cnt - off0);
     uint64_t rec[kBItems];
@@ -523,23 +577,21 @@ __global__ void __launch_bounds__(kBThreads, 3)
     for (int q = 0; q < kBItems; ++q) {
       const uint32_t e = (q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
       const uint32_t f = (uint32_t)(rec[q] >> fshift) & fmask;
-      pk[q] = e < nrec ? (f << 16) | atomicAdd(&sm.hist[f], 1u) : 0xFFFFFFFFu;
+      pk[q] = e < nrec && !is_filler(rec[q]) ? (f << 16) | atomicAdd(&sm.cnt[f], 1u) : 0xFFFFFFFFu;
     }
     __syncthreads();
-    bin_reserve(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
+    bin_reserve<true>(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
-      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
-    __syncthreads();
-    bin_write(nrec, w.binf + (uint64_t)c * pl.F2 * pl.capf, sm, pol, [&](uint64_t rc, uint32_t p) {
-      uint32_t f = 0;  // the fine bin of sorted position p
-      while (f + 1 < pl.F2 && sm.hist[f + 1] <= p) ++f;
+      if (pk[q] != 0xFFFFFFFFu) bin_place<true>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
+    bin_write(pl.F2, w.binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](uint64_t rc, uint32_t f) {
       const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
       resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
     });
     __syncthreads();
   }
+  bulk_wait_all();
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
 }
 
@@ -697,9 +749,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
           uint32_t vm = 0;  // bit q: record q valid
 #pragma unroll
           for (int q = 0; q < K; ++q) {
-            const bool v = kbase + (q0 + q) * 32 < len;
+            rc[q] = kbase + (q0 + q) * 32 < len ? rs[(q0 + q) * 32] : kFiller;
+            const bool v = !is_filler(rc[q]);  // past the chunk, or run padding
             vm |= (uint32_t)v << q;
-            rc[q] = v ? rs[(q0 + q) * 32] : 0;
             const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
             // queries snapshot all buckets up front; mutations snapshot right
             // before their CAS (a stale snapshot costs a whole-warp retry)
