@@ -486,7 +486,7 @@ static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, ui
 // ---------------------------------------------------------------------------
 
 struct RLayout {
-  uint64_t cnt1, cntf, bin_ctr_end, n_miss, ctr_end, bin1, binf, miss, bits, total;
+  uint64_t cnt1, cntf, bin_ctr_end, n_miss, mode, ctr_end, bin1, binf, miss, bits, total;
 };
 
 static uint32_t ceil_log2(uint64_t x) {
@@ -563,7 +563,8 @@ static RLayout rlayout_for(const RPlan& pl, uint64_t n, int op) {
   L.cntf = align256(L.cnt1 + pl.R1 * cs);
   L.bin_ctr_end = align256(L.cntf + pl.R * cs);  // bin counters: zeroed again between the phases
   L.n_miss = L.bin_ctr_end;
-  L.ctr_end = align256(L.n_miss + 4ull * kMaxProbeGrid);
+  L.mode = L.n_miss + 4ull * kMaxProbeGrid;
+  L.ctr_end = align256(L.mode + 8);
   L.bin1 = L.ctr_end;
   L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
   L.miss = align256(L.binf + pl.R * pl.capf * 8);
@@ -579,6 +580,7 @@ static RWork rwork_view(void* ws, const RLayout& L, const RPlan& pl) {
   w.cnt1 = (uint32_t*)(b + L.cnt1);
   w.cntf = (uint32_t*)(b + L.cntf);
   w.n_miss = (uint32_t*)(b + L.n_miss);
+  w.mode = (uint32_t*)(b + L.mode);
   w.bin1 = (uint64_t*)(b + L.bin1);
   w.binf = (uint64_t*)(b + L.binf);
   w.miss = (uint4*)(b + L.miss);
@@ -608,7 +610,15 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
                       cudaStream_t s) {
   RWork w = rwork_view(ws, L, pl);
   if (cudaMemsetAsync(ws, 0, L.ctr_end, s) != cudaSuccess) return cuda_error();  // bin + miss counters
-  if (OP != OP_INSERT) {  // all-true: only final negatives clear their bit
+  if (OP == OP_QUERY) {  // starting value of the results from a sample of the batch
+    region_sample_kernel<F, WPB, POL><<<kSample / 256, 256, 0, s>>>(g, words, keys, n, hashed, w.mode);
+    int st0 = status();
+    if (st0) return st0;
+    fill_bits_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, (n + 31) / 32, n, w.mode);
+    if ((st0 = status())) return st0;
+    sk.bits = w.bits;
+  } else if (OP == OP_DELETE) {  // all-true: only keys found in neither bucket clear their bit
+    if (cudaMemsetAsync(w.mode, 1, 4, s) != cudaSuccess) return cuda_error();
     if (cudaMemsetAsync(w.bits, 0xFF, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
     sk.bits = w.bits;
   }

@@ -265,6 +265,9 @@ struct RWork {
   uint32_t* n_miss; // [grid] entries per segment
   uint64_t seg;     // entries per segment
   uint32_t* bits;   // [ceil(n/32)] result bitmap (query / delete)
+  uint32_t* mode;   // [2] mode[0] nonzero: results start all-true and final negatives clear their bit;
+                    // zero: results start all-false and hits set theirs (query batches
+                    // sampled as mostly negative)
 };
 
 // What to do with a record that finds its bin full (adversarial inputs only):
@@ -272,7 +275,8 @@ struct RWork {
 // resident in shared memory while the bin / split kernels run.
 template <int OP, int F, int WPB, int POL>
 __device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, uint64_t rec, uint64_t bucket,
-                                               const Sink& sk, uint32_t& n_ok, uint32_t& n_alt) {
+                                               const Sink& sk, const uint32_t* w_mode, uint32_t& n_ok,
+                                               uint32_t& n_alt) {
   using Lg = Logic<OP, F, WPB, POL>;
   const uint32_t idx = (uint32_t)(rec >> 32);
   const uint64_t fp = rec & ((1ull << g.payload_bits) - 1u);
@@ -290,8 +294,9 @@ __device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, ui
   }
   if (done) {
     if (OP != OP_QUERY) ++n_ok;
+    if (OP == OP_QUERY && !*w_mode) set_bit(sk.bits, idx);
   } else if (OP != OP_INSERT) {
-    clear_bit(sk.bits, idx);  // results start all-true (region schedule)
+    if (*w_mode) clear_bit(sk.bits, idx);
   } else {
     const uint64_t k = sk.keys[idx];
     enqueue_evict_one(sk, idx, sk.hashed ? k : xxh64(k, g.seed));
@@ -522,7 +527,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       if (pk[q] != 0xFFFFFFFFu) bin_place<kBulk>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
     auto ovf = [&](uint64_t rc, uint32_t b) {
       const uint64_t bucket = ((uint64_t)b << pl.lrbc) + ((rc >> pl.pb) & lmask);
-      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
+      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
     if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
     else bin_write_coalesced(pl.R1, (uint32_t)min((uint64_t)KT, n - t0), w.bin1, pl.cap1, sm, pol, ovf);
@@ -587,7 +592,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       if (pk[q] != 0xFFFFFFFFu) bin_place<true>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
     bin_write(pl.F2, w.binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](uint64_t rc, uint32_t f) {
       const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
-      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, n_ok, n_alt);
+      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
     });
     __syncthreads();
   }
@@ -674,6 +679,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rb = 1u << pl.lrb;
   constexpr uint32_t bbytes = WPB * 8;
+  const bool dflt = OP == OP_QUERY ? *w.mode != 0 : true;  // results' starting value (see RWork::mode)
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(full + s, 1);
@@ -767,7 +773,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint32_t idx = (uint32_t)(rc[q] >> 32);
             if constexpr (OP == OP_QUERY) {
               const bool hit = match_any<F, WPB, POL>(wv[q], fp);
-              if (PHASE == 2 && !hit) clear_bit(sk.bits, idx);  // a final negative
+              if (hit && !dflt) set_bit(sk.bits, idx);
+              if (PHASE == 2 && !hit && dflt) clear_bit(sk.bits, idx);  // a final negative
               if (PHASE == 1 && !hit) {
                 nm |= 1u << q;
                 uint64_t cc;
@@ -837,6 +844,43 @@ __global__ void __launch_bounds__(kPThreads, 1)
   }
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);  // (synchronizes the block)
   if (PHASE == 1 && tid == 0) w.n_miss[blockIdx.x] = s_miss[0];
+}
+
+// Query batches: estimate the fraction of positive keys from an evenly spaced
+// sample of kSample keys (one direct lookup per thread on the global table)
+// and pick the result bitmap's starting value, so that only the minority
+// outcome costs an L2 atomic.  mode[1] accumulates the sample's hits.
+constexpr uint32_t kSample = 8192;
+
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(256) region_sample_kernel(Geo g, const uint64_t* __restrict__ words,
+                                                            const uint64_t* __restrict__ keys, uint64_t n,
+                                                            bool hashed, uint32_t* mode) {
+  using Lg = Logic<OP_QUERY, F, WPB, POL>;
+  const uint64_t ns = n < kSample ? n : kSample;
+  const uint32_t k = blockIdx.x * blockDim.x + threadIdx.x;
+  bool hit = false;
+  if (k < ns) {
+    const uint64_t i = (uint64_t)k * n / ns;
+    uint64_t fp, i1, i2;
+    place<POL>(hashed ? keys[i] : xxh64(keys[i], g.seed), g, fp, i1, i2);
+    uint64_t* w = const_cast<uint64_t*>(words);
+    hit = Lg::first(w, i1, fp, g) || Lg::second(w, i2, fp, g);
+  }
+  const uint32_t c = __popc(__ballot_sync(0xffffffffu, hit));
+  if ((threadIdx.x & 31) == 0 && c) atomicAdd(mode + 1, c);
+}
+
+// Result bitmap starting value: all-true for a batch sampled as mostly
+// positive (mode[0] = 1), all-false otherwise.
+__global__ void __launch_bounds__(256) fill_bits_kernel(uint32_t* __restrict__ bits, uint64_t nw, uint64_t n,
+                                                        uint32_t* mode) {
+  const uint64_t ns = n < kSample ? n : kSample;
+  const bool dflt = 2ull * mode[1] >= ns;
+  const uint32_t v = dflt ? ~0u : 0u;
+  if (blockIdx.x == 0 && threadIdx.x == 0) mode[0] = dflt;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < nw; i += (uint64_t)gridDim.x * blockDim.x)
+    bits[i] = v;
 }
 
 // bitmap -> one byte per key, and (queries) the hit count

@@ -23,16 +23,18 @@ for d in ours:
     m = re.search(r"ckf::(\w+)<([^>]*)>", d["name"]) or re.search(r"ckf::(\w+)", d["name"])
     d["short"] = m.group(1)
     args = [a.strip() for a in m.group(2).split(",")] if m.lastindex and m.lastindex > 1 else []
-    d["op"] = int(args[0]) if args and m.group(1).startswith(("tile", "region")) else None
+    d["op"] = (int(args[0]) if args and m.group(1).startswith(("tile", "region"))
+               and m.group(1) != "region_sample_kernel" else None)
     # a new op call starts at its first pass: the keys' bin kernel (region SRC_KEYS = 0) or a direct kernel
-    d["start"] = (d["short"] == "tile_bin_kernel" or (d["short"] == "region_bin_kernel" and args[-1] == "0")
+    d["start"] = (d["short"] in ("tile_bin_kernel", "region_sample_kernel")
+                  or (d["short"] == "region_bin_kernel" and args[-1] == "0")
                   or d["short"] in ("insert_kernel", "query_kernel", "delete_kernel"))
 
 
 def op_of(d):
     if d["short"] in ("insert_kernel", "evict_kernel"):
         return "insert"
-    if d["short"] == "query_kernel":
+    if d["short"] in ("query_kernel", "region_sample_kernel"):
         return "query"
     if d["short"] == "delete_kernel":
         return "delete"
@@ -44,7 +46,8 @@ def op_of(d):
 groups = []
 for d in ours:
     o = op_of(d)
-    if d["start"] or not groups:
+    after_sample = bool(groups) and groups[-1][1][-1]["short"] in ("region_sample_kernel", "fill_bits_kernel")
+    if (d["start"] and not after_sample) or not groups:
         groups.append((o, [d]))
     else:
         groups[-1][1].append(d)
