@@ -532,8 +532,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   pl.R1 = (uint32_t)R1;
   pl.R = pl.R1 * pl.F2;
   pl.pb = pb;
-  const double recs = (double)n;
-  (void)op;
+  const double recs = (double)n * (op == CKF_OP_QUERY ? 2.0 : 1.0);  // dual query records
   // + run padding: at most one filler per bin per tile of the pass that fills it
   // (bin: ceil(n / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
   const uint64_t tiles1 = (n + kBTile - 1) / kBTile + (uint64_t)kMaxProbeGrid;

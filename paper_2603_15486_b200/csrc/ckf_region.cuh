@@ -455,13 +455,16 @@ __global__ void __launch_bounds__(kBThreads, 3)
                       RWork w, Sink sk, long long* occ) {
   extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
   BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
-  constexpr int KT = kBTile;  // items per tile
+  // dual: a query batch sampled as mostly negative gets an i1 AND an i2 record
+  // per key here (no phase 2); the tile then holds kBTile / 2 keys
+  const bool dual = OP == OP_QUERY && SRC == SRC_KEYS && w.mode[0] == 0;
+  const uint64_t KT = dual ? kBTile / 2 : kBTile;  // keys (items) per tile
   const uint64_t pol = evict_first_policy();
   const uint32_t lmask = (1u << pl.lrbc) - 1u;
   const uint64_t n = SRC == SRC_KEYS ? n_keys : w.n_miss[blockIdx.y];
   const uint4* ms = w.miss + (uint64_t)blockIdx.y * w.seg;
   uint32_t n_ok = 0, n_alt = 0;
-  for (uint64_t t0 = blockIdx.x * (uint64_t)KT; t0 < n; t0 += (uint64_t)gridDim.x * KT) {
+  for (uint64_t t0 = blockIdx.x * KT; t0 < n; t0 += (uint64_t)gridDim.x * KT) {
     if (threadIdx.x == 0) {
       const uint64_t nx = t0 + (uint64_t)gridDim.x * KT;
       if (nx < n && n - nx >= 2) {
@@ -477,7 +480,9 @@ __global__ void __launch_bounds__(kBThreads, 3)
 #pragma unroll
       for (int q = 0; q < kBItems / 2; ++q) {
         const uint64_t i = t0 + (uint64_t)q * 2 * kBThreads + 2 * threadIdx.x;
-        if (i + 1 < n) {
+        if (dual && q >= kBItems / 4) {
+          kk[2 * q] = kk[2 * q + 1] = 0;
+        } else if (i + 1 < n) {
           asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                        : "=l"(kk[2 * q]), "=l"(kk[2 * q + 1])
                        : "l"(keys + i), "l"(pol));
@@ -489,6 +494,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       __syncthreads();
 #pragma unroll
       for (int q = 0; q < kBItems; ++q) {
+        if (dual && q >= kBItems / 2) continue;  // filled with key q - kBItems/2's i2 record
         const uint64_t i = t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
         const uint64_t h = hashed ? kk[q] : xxh64(kk[q], g.seed);
         const uint64_t fp0 = (h >> 32) & ((1ull << g.payload_bits) - 1u);
@@ -497,6 +503,13 @@ __global__ void __launch_bounds__(kBThreads, 3)
         const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
         rec[q] = rpack(i, 0u, i1 & lmask, fp, pl.pb);
         pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
+        if (q < kBItems / 2 && dual) {
+          uint64_t cc;
+          const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, cc);
+          const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
+          rec[q + kBItems / 2] = rpack(i, 1u, i2 & lmask, fp, pl.pb);
+          pk[q + kBItems / 2] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
+        }
       }
     } else {
       __syncthreads();  // hist zeroed
@@ -530,7 +543,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
     if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
-    else bin_write_coalesced(pl.R1, (uint32_t)min((uint64_t)KT, n - t0), w.bin1, pl.cap1, sm, pol, ovf);
+    else bin_write_coalesced(pl.R1, (uint32_t)(min(KT, n - t0) * (dual ? 2 : 1)), w.bin1, pl.cap1, sm, pol, ovf);
     __syncthreads();
   }
   bulk_wait_all();
@@ -775,7 +788,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
               const bool hit = match_any<F, WPB, POL>(wv[q], fp);
               if (hit && !dflt) set_bit(sk.bits, idx);
               if (PHASE == 2 && !hit && dflt) clear_bit(sk.bits, idx);  // a final negative
-              if (PHASE == 1 && !hit) {
+              if (PHASE == 1 && !hit && !dflt) {  // dual records: the i2 record is binned already
+                n_alt += !((rc[q] >> 31) & 1u);
+              } else if (PHASE == 1 && !hit) {
                 nm |= 1u << q;
                 uint64_t cc;
                 i2[q] = alt_index<POL>(b0 + loc, fp, 0, g, cc);

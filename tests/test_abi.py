@@ -97,8 +97,9 @@ def test_workspace_sizing():
     wq = L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_QUERY, 0)
     wi = L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_INSERT, 0)
     # region schedule: coarse- and fine-binned 8 B records plus a 16 B miss
-    # entry per key (+ the result bitmap for query)
-    assert 32 * n <= wi < 34 * n and wq == wi + ((n + 31) // 32 * 4 + 255) // 256 * 256
+    # entry per key; queries also size the bins for two records per key (dual
+    # mode) and add the result bitmap
+    assert 32 * n <= wi < 34 * n and 1.5 * wi < wq < 2.5 * wi
     small = FilterConfig(bucket_count=1 << 10).ckf_params()
     assert L.ckf_workspace_bytes(ctypes.byref(small), 100_000, _lib.OP_QUERY, 0) == 0  # L2-resident
     assert L.ckf_workspace_bytes(ctypes.byref(small), 100_000, _lib.OP_QUERY, _lib.FORCE_TILED) > 0

@@ -1,0 +1,124 @@
+"""GPU tests aimed at the shared-memory region schedule (ckf_region.cuh).
+
+`tiled=True` forces the batch schedule onto small tables (>= 16 fine regions),
+so these run in seconds and still cross every region / bin boundary:
+  * query results are bit-exact against the oracle for batches the device
+    samples as mostly positive (result bitmap starts all-true), mostly
+    negative (starts all-false) and mixed;
+  * adversarial keys whose primary buckets all fall into one region overflow
+    the coarse and fine bins (direct resolution path) and still give the
+    reference's insert-success count, no false negatives, exact occupancy and
+    a clean delete;
+  * duplicate keys (one bucket pair) fail exactly as many times as in the
+    reference.
+"""
+
+from __future__ import annotations
+
+import numpy as np
+import pytest
+import torch
+
+import oracle
+from paper_2603_15486_b200 import CuckooFilter, FilterConfig, _lib
+
+pytestmark = pytest.mark.gpu
+
+CASES = [(16, 16, "xor"), (16, 16, "offset"), (8, 16, "xor"), (16, 32, "xor")]
+
+
+def _cfg(f, b, pol, m=1 << 12, ev="bfs"):
+    if pol == "offset":
+        m = m - 3  # non-power-of-two m (offset policy only)
+    return FilterConfig(bucket_count=m, fingerprint_bits=f, bucket_slots=b, policy=pol, eviction=ev, seed=3)
+
+
+@pytest.mark.parametrize("f,b,pol", CASES)
+@pytest.mark.parametrize("pos_frac", [1.0, 0.9, 0.5, 0.1, 0.0])
+def test_region_query_exact_vs_oracle(f, b, pol, pos_frac):
+    cfg = _cfg(f, b, pol)
+    rng = np.random.default_rng(11)
+    keys = rng.integers(0, 1 << 62, size=int(0.9 * cfg.total_slots), dtype=np.uint64)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    ok, _, _ = ref.insert_batch(keys)
+    filt = CuckooFilter(cfg, tiled=True)
+    filt.words_device.copy_(torch.from_numpy(ref.words.view(np.int64)))
+    filt._occ.fill_(int(ok.sum()))
+    n = 200_000
+    npos = int(pos_frac * n)
+    q = np.concatenate([rng.choice(keys, npos), rng.integers(1 << 62, 1 << 63, size=n - npos, dtype=np.uint64)])
+    rng.shuffle(q)
+    l0 = _lib.kernel_launches()
+    got = filt.query_batch(q)
+    # sample, fill, bin, split, probe, miss bin, split, probe, expand: the region schedule ran
+    assert _lib.kernel_launches() - l0 >= 9
+    assert np.array_equal(got, ref.query_batch(q))
+    c = filt.last_counters()
+    assert c["n_ok"] == int(got.sum())
+
+
+def _same_region_keys(cfg, want: int, region_buckets: int, seed: int = 5) -> np.ndarray:
+    """Keys whose primary bucket lies in [0, region_buckets)."""
+    ocfg = oracle.cfg_from(cfg)
+    rng = np.random.default_rng(seed)
+    out = []
+    while sum(len(o) for o in out) < want:
+        k = rng.integers(0, 1 << 63, size=1 << 20, dtype=np.uint64)
+        _, i1, _ = oracle.place_batch(ocfg, k)
+        out.append(k[i1 < region_buckets])
+    return np.concatenate(out)[:want]
+
+
+@pytest.mark.parametrize("pol", ["xor", "offset"])
+def test_region_bin_overflow_adversarial(pol):
+    cfg = _cfg(16, 16, pol, m=1 << 13)
+    # every primary bucket in the first 1/16 of the table: that coarse / fine
+    # bin receives ~16x its capacity and the overflow resolves on the direct path
+    keys = _same_region_keys(cfg, want=int(0.45 * (cfg.bucket_count // 16) * cfg.bucket_slots * 2),
+                             region_buckets=cfg.bucket_count // 16)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    rok, _, _ = ref.insert_batch(keys)
+    filt = CuckooFilter(cfg, tiled=True)
+    res = filt.insert_batch(keys)
+    assert res.n_failed == int((~rok).sum())
+    assert len(filt) == res.n_ok == int(np.count_nonzero(filt.stored_tags()))
+    stored = keys[res.ok]
+    assert filt.query_batch(stored).all(), "false negative"
+    d = filt.delete_batch(stored)
+    assert d.all() and len(filt) == 0 and int(np.count_nonzero(filt.words)) == 0
+
+
+def test_region_duplicates_fail_like_reference():
+    cfg = _cfg(16, 16, "xor", m=1 << 12)
+    rng = np.random.default_rng(2)
+    base = rng.integers(0, 1 << 62, size=20_000, dtype=np.uint64)
+    dup = np.repeat(np.uint64(0xDEADBEEF), 40)  # 40 copies of one key: 32 slots in its pair
+    keys = np.concatenate([base, dup])
+    rng.shuffle(keys)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    rok, _, _ = ref.insert_batch(keys)
+    filt = CuckooFilter(cfg, tiled=True)
+    res = filt.insert_batch(keys)
+    assert res.n_failed == int((~rok).sum()) >= 8
+    assert filt.query_batch(base).all()
+    # deleting 40 copies removes exactly the stored ones
+    d = filt.delete_batch(dup)
+    assert int(d.sum()) == int(res.ok[keys == np.uint64(0xDEADBEEF)].sum())
+
+
+def test_region_delete_absent_keys_report_false():
+    cfg = _cfg(16, 16, "xor", m=1 << 12)
+    rng = np.random.default_rng(4)
+    keys = rng.integers(0, 1 << 32, size=50_000, dtype=np.uint64)
+    filt = CuckooFilter(cfg, tiled=True)
+    filt.insert_batch(keys)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    ref.insert_batch(keys)
+    absent = rng.integers(1 << 40, 1 << 62, size=200_000, dtype=np.uint64)
+    got = filt.delete_batch(absent)
+    want = ref.delete_batch(absent)
+    # an absent key whose fingerprint matches a stored tag deletes it (reference
+    # semantics, FPR-rate); only two absent keys racing for one tag could differ
+    assert abs(int(got.sum()) - int(want.sum())) <= 2
+    assert int(got.sum()) < 200
+    assert len(filt) == len(keys) - int(got.sum())
