@@ -198,13 +198,15 @@ template <int F, int WPB, int POL>
 __global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
                                                        int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
                                                        ckf_record* __restrict__ rec, uint64_t cap,
-                                                       ckf_counters* ctr, long long* occ) {
+                                                       ckf_counters* ctr, long long* occ,
+                                                       const uint64_t* __restrict__ keys, bool hashed) {
   const unsigned long long queued = *(volatile unsigned long long*)&ctr->n_queued;
   const uint64_t cnt = queued < cap ? queued : cap;
   uint32_t n_ok = 0;
   for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < cnt; r += (uint64_t)gridDim.x * blockDim.x) {
     const uint64_t i = rec[r].index;
-    const uint64_t h = rec[r].lost;  // the direct pass parks the key hash here
+    uint64_t h = rec[r].lost;  // the key hash parked by the queueing pass, or kRehash
+    if (h == kRehash) h = load_hash(keys, i, g.seed, hashed);
     uint64_t fp, i1, i2;
     place<POL>(h, g, fp, i1, i2);
     Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
@@ -763,7 +765,8 @@ struct InsertOp {
       // the queue length is only known on the device: a fixed full-residency grid
       // strides over it (empty queues exit immediately)
       unsigned egrid = (unsigned)sm_count() * 4;
-      evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ);
+      evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ,
+                                                         a.keys, a.hashed);
       st = status();
     }
     return st;

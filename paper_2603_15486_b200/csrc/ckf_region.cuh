@@ -89,6 +89,44 @@ __device__ __forceinline__ void lds_bucket(uint32_t a, uint64_t (&w)[WPB]) {
   }
 }
 
+// Bank-spread bucket gather: lane l fetches the bucket's 16 B chunks starting
+// at chunk (l mod chunks), so the lanes of one LDS.128 split over different
+// bank quads (random 32 B gathers otherwise pay ~3x in bank conflicts).
+// kOrdered: put the words back in bucket order (mutations); queries OR over
+// the words and skip that.
+template <int WPB, bool kOrdered>
+__device__ __forceinline__ void lds_bucket_spread(uint32_t a, uint64_t (&w)[WPB]) {
+  if constexpr (WPB < 4) {
+    lds_bucket<WPB>(a, w);
+  } else {
+    constexpr int C = WPB / 2;  // 16 B chunks
+    const int r = (int)(threadIdx.x & (C - 1));
+    uint64_t t[WPB];
+#pragma unroll
+    for (int k = 0; k < C; ++k) {
+      const uint32_t off = (uint32_t)(((k + r) & (C - 1)) * 16);
+      asm volatile("ld.shared.v2.u64 {%0,%1}, [%2];" : "=l"(t[2 * k]), "=l"(t[2 * k + 1]) : "r"(a + off) : "memory");
+    }
+    if constexpr (kOrdered) {  // chunk k of t is bucket chunk (k + r) mod C
+#pragma unroll
+      for (int c = 0; c < C; ++c) {
+        uint64_t lo = t[0], hi = t[1];
+#pragma unroll
+        for (int k = 1; k < C; ++k)
+          if (((k + r) & (C - 1)) == c) {
+            lo = t[2 * k];
+            hi = t[2 * k + 1];
+          }
+        w[2 * c] = lo;
+        w[2 * c + 1] = hi;
+      }
+    } else {
+#pragma unroll
+      for (int j = 0; j < WPB; ++j) w[j] = t[j];
+    }
+  }
+}
+
 __device__ __forceinline__ uint64_t cas_shared(uint32_t a, uint64_t cmp, uint64_t val) {
   uint64_t old;
   asm volatile("atom.shared.cas.b64 %0, [%1], %2, %3;" : "=l"(old) : "r"(a), "l"(cmp), "l"(val) : "memory");
@@ -633,11 +671,13 @@ __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
 __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;" ::"n"(kPConsumers) : "memory"); }
 
 // Queue unplaced inserts for the eviction pass: one reservation per warp for
-// the whole sub-batch, then the keys are re-read (scattered, ~4 % of keys)
-// and hashed.  Whole warp, converged.
+// the whole sub-batch.  Only the key index is queued (hash field = kRehash);
+// the eviction kernel re-reads and hashes the key, so this smem-bound kernel
+// never waits on the scattered key reads.  Whole warp, converged.
+constexpr uint64_t kRehash = ~0ull;
+
 template <int K>
-__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K],
-                                                    const Geo& g) {
+__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K]) {
   const int lane = threadIdx.x & 31;
   const uint32_t c = __popc(nm);
   uint32_t incl = c;
@@ -652,14 +692,11 @@ __device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm,
   if (lane == 31) base = atomicAdd(&sk.ctr->n_queued, (unsigned long long)total);
   base = __shfl_sync(0xffffffffu, base, 31);
   uint64_t pos = base + incl - c;
-  uint64_t k[K];
-#pragma unroll
-  for (int q = 0; q < K; ++q) k[q] = ((nm >> q) & 1u) ? sk.keys[rc[q] >> 32] : 0;
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     if (!((nm >> q) & 1u)) continue;
     const uint32_t idx = (uint32_t)(rc[q] >> 32);
-    if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, sk.hashed ? k[q] : xxh64(k[q], g.seed), 0u, 0u};
+    if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, kRehash, 0u, 0u};
     else if (sk.ok) sk.ok[idx] = 0;
     ++pos;
   }
@@ -774,7 +811,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
             // queries snapshot all buckets up front; mutations snapshot right
             // before their CAS (a stale snapshot costs a whole-warp retry)
-            if (OP == OP_QUERY && v) lds_bucket<WPB>(tab_a + loc * bbytes, wv[q]);
+            if (OP == OP_QUERY && v) lds_bucket_spread<WPB, false>(tab_a + loc * bbytes, wv[q]);
           }
           uint32_t nm = 0;  // bit q: record q not resolved here
           uint64_t i2[K];
@@ -798,7 +835,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
             } else {
               const uint32_t a = tab_a + loc * bbytes;
               const uint64_t tag = PHASE == 1 ? fp : (POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp);
-              lds_bucket<WPB>(a, wv[q]);
+              lds_bucket<WPB>(a, wv[q]);  // (spread order measured slower here: instruction-bound)
               const bool done =
                   OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv[q]) : smem_remove<F, WPB>(a, tag, wv[q]);
               n_ok += done;
@@ -836,7 +873,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
                                       (uint32_t)(i2[q] >> 32));
             }
           } else if constexpr (OP == OP_INSERT && PHASE == 2) {
-            enqueue_evict_batch<K>(sk, nm, rc, g);
+            enqueue_evict_batch<K>(sk, nm, rc);
           }
         }
         __syncwarp();
