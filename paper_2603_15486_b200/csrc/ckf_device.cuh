@@ -412,7 +412,7 @@ __device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_
 // start from those snapshots.  Decisions are taken in exactly the reference
 // order (first candidate with room, K:407-414), so the sequential parity mode
 // stays bit-identical.
-constexpr int kEvictFetch = 4;
+constexpr int kEvictFetch = 2;
 
 template <int F>
 __device__ __forceinline__ bool lane_cas_from(uint64_t* p, int lane, uint64_t expect, uint64_t repl, uint64_t w) {

@@ -631,7 +631,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   constexpr uint32_t kBinSmem = sizeof(BinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
-  allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmem);
+  allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmemBulk);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmem);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
   int st;
@@ -639,7 +639,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, 3), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, n, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
@@ -648,7 +648,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * 3 + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, 0, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;

@@ -357,12 +357,13 @@ __device__ __forceinline__ bool is_filler(uint64_t rc) { return (uint32_t)(rc >>
 
 struct BinSmem {
   uint64_t rec[kBTile + kRMaxCoarse];  // sorted tile (bulk writer: runs padded to even length)
-  uint32_t dst[kBTile];                // coalesced writer: destination slot of each sorted record
   uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
   uint32_t start[kRMaxCoarse];         // run start in rec (even)
   uint32_t gbase[kRMaxCoarse];         // run start in the bin (even)
   uint32_t warp_sums[kBThreads / 32];
+  uint32_t dst[kBTile];                // coalesced writer only (last: bulk-only kernels omit it)
 };
+constexpr uint32_t kBinSmemBulk = sizeof(BinSmem) - sizeof(uint32_t) * kBTile;
 
 // sm.cnt (records per bin) -> sm.start (exclusive scan of the padded run
 // lengths) and sm.gbase (one global reservation per non-empty bin)
