@@ -148,6 +148,18 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                uint8_t* out, ckf_counters* counters, long long* occupancy, void* workspace,
                uint64_t workspace_bytes, unsigned flags, void* stream);
 
+/* k-mer ingestion (replaces swarcuckoo/kmer.py:48-95 stream_kmers' packing
+ * loop).  seq: device bytes of the FASTA records' sequence lines, each record's
+ * lines concatenated, one separator byte (any byte outside ACGTacgt) between
+ * records.  Every length-k window (1 <= k <= 31) of A/C/G/T bases (either
+ * case) that crosses no other byte is packed two bits per base, leftmost base
+ * most significant, and written to out[] in sequence order; out needs room for
+ * len - k + 1 keys.  *n_out (device) receives the count.  workspace: at least
+ * ckf_kmer_workspace_bytes(len) device bytes. */
+uint64_t ckf_kmer_workspace_bytes(uint64_t len);
+int ckf_kmers(const uint8_t* seq, uint64_t len, uint32_t k, uint64_t* out,
+              unsigned long long* n_out, void* workspace, uint64_t workspace_bytes, void* stream);
+
 /* Host-compiled copies of the shared device semantics (same source as the
  * kernels); used by derive_placement() and by the CPU parity tests. */
 uint64_t ckf_host_hash(uint64_t key, uint64_t seed);

@@ -830,6 +830,92 @@ static bool params_ok(const ckf_params* p) {
 
 }  // namespace ckf
 
+// ---------------------------------------------------------------------------
+// k-mer ingestion (reference kmer.py:48-95)
+// ---------------------------------------------------------------------------
+//
+// `seq` holds the records' sequence bytes with a separator byte between
+// records.  A window of k bases is emitted iff none of its bytes is outside
+// ACGTacgt (separators, N, ...), packed two bits per base with the leftmost
+// base most significant -- the reference's rolling `value = (value << 2 |
+// code) & mask` with `fill` reset on an ambiguous base.  Two passes over
+// kKmerChunk-position chunks (count, then emit at scanned offsets) keep the
+// output in sequence order.
+
+constexpr uint32_t kKmerChunk = 1024;
+
+__device__ __forceinline__ uint32_t base_code(uint8_t c) {
+  // A C G T (either case) -> 0..3, anything else -> 4
+  const uint8_t u = c & 0xDF;
+  return u == 'A' ? 0u : u == 'C' ? 1u : u == 'G' ? 2u : u == 'T' ? 3u : 4u;
+}
+
+// EMIT = false: counts[c] = windows ending in chunk c; true: write them at offs[c]
+template <bool EMIT>
+__global__ void __launch_bounds__(256) kmer_chunk_kernel(const uint8_t* __restrict__ seq, uint64_t len, uint32_t k,
+                                                         uint32_t* __restrict__ counts,
+                                                         const uint64_t* __restrict__ offs,
+                                                         uint64_t* __restrict__ out) {
+  const uint64_t nch = (len + kKmerChunk - 1) / kKmerChunk;
+  const uint64_t mask = k >= 32 ? ~0ull : ((1ull << (2 * k)) - 1u);
+  for (uint64_t c = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; c < nch; c += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t s = c * kKmerChunk, e = min(len, s + kKmerChunk);
+    uint64_t p = s >= k - 1 ? s - (k - 1) : 0;
+    uint64_t value = 0, o = EMIT ? offs[c] : 0;
+    uint32_t fill = 0, cnt = 0;
+    for (; p < e; ++p) {
+      const uint32_t code = base_code(__ldg(seq + p));
+      if (code > 3u) {
+        value = 0;
+        fill = 0;
+        continue;
+      }
+      value = ((value << 2) | code) & mask;
+      fill = fill < k ? fill + 1 : k;
+      if (fill == k && p >= s) {
+        if (EMIT) out[o++] = value;
+        else ++cnt;
+      }
+    }
+    if (!EMIT) counts[c] = cnt;
+  }
+}
+
+// exclusive scan of the chunk counts (one block) -> offsets, total -> *n_out
+__global__ void __launch_bounds__(1024) kmer_scan_kernel(const uint32_t* __restrict__ counts, uint64_t nch,
+                                                         uint64_t* __restrict__ offs, unsigned long long* n_out) {
+  __shared__ uint64_t wsum[32];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t per = (nch + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min((uint64_t)tid * per, nch), hi = min(lo + per, nch);
+  uint64_t sum = 0;
+  for (uint64_t i = lo; i < hi; ++i) sum += counts[i];
+  uint64_t x = sum;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+    if (lane >= d) x += y;
+  }
+  if (lane == 31) wsum[wid] = x;
+  __syncthreads();
+  if (wid == 0) {
+    uint64_t v = lane < (int)(blockDim.x / 32) ? wsum[lane] : 0, t = v;
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, t, d);
+      if (lane >= d) t += y;
+    }
+    wsum[lane] = t - v;
+    if (lane == 31) *n_out = t;
+  }
+  __syncthreads();
+  uint64_t run = wsum[wid] + x - sum;
+  for (uint64_t i = lo; i < hi; ++i) {
+    offs[i] = run;
+    run += counts[i];
+  }
+}
+
 // ===========================================================================
 // C ABI
 // ===========================================================================
@@ -977,6 +1063,30 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,
                (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, keys, workspace, workspace_bytes)};
   return dispatch3<DeleteOp>(p, words, a);
+}
+
+uint64_t ckf_kmer_workspace_bytes(uint64_t len) {
+  const uint64_t nch = (len + kKmerChunk - 1) / kKmerChunk;
+  return align256(nch * 4) + align256(nch * 8);
+}
+
+int ckf_kmers(const uint8_t* seq, uint64_t len, uint32_t k, uint64_t* out, unsigned long long* n_out,
+              void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (k < 1 || k > 31 || !n_out) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (len == 0) return cudaMemsetAsync(n_out, 0, 8, s) == cudaSuccess ? CKF_OK : cuda_error();
+  if (!seq || !out || !workspace || workspace_bytes < ckf_kmer_workspace_bytes(len)) return CKF_EINVAL;
+  const uint64_t nch = (len + kKmerChunk - 1) / kKmerChunk;
+  uint32_t* counts = (uint32_t*)workspace;
+  uint64_t* offs = (uint64_t*)((char*)workspace + align256(nch * 4));
+  const unsigned grid = grid_for(nch, 256, 8);
+  kmer_chunk_kernel<false><<<grid, 256, 0, s>>>(seq, len, k, counts, nullptr, nullptr);
+  int st = status();
+  if (st) return st;
+  kmer_scan_kernel<<<1, 1024, 0, s>>>(counts, nch, offs, n_out);
+  if ((st = status())) return st;
+  kmer_chunk_kernel<true><<<grid, 256, 0, s>>>(seq, len, k, nullptr, offs, out);
+  return status();
 }
 
 uint64_t ckf_host_hash(uint64_t key, uint64_t seed) { return xxh64(key, seed); }

@@ -358,15 +358,14 @@ __device__ __forceinline__ bool is_filler(uint64_t rc) { return (uint32_t)(rc >>
 struct BinSmem {
   uint64_t rec[kBTile + kRMaxCoarse];  // sorted tile (bulk writer: runs padded to even length)
   uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
-  uint32_t start[kRMaxCoarse];         // run start in rec (even)
-  uint32_t gbase[kRMaxCoarse];         // run start in the bin (even)
+  uint2 sg[kRMaxCoarse];               // {run start in rec, run start in the bin} (bulk: both even)
   uint32_t warp_sums[kBThreads / 32];
   uint32_t dst[kBTile];                // coalesced writer only (last: bulk-only kernels omit it)
 };
 constexpr uint32_t kBinSmemBulk = sizeof(BinSmem) - sizeof(uint32_t) * kBTile;
 
-// sm.cnt (records per bin) -> sm.start (exclusive scan of the padded run
-// lengths) and sm.gbase (one global reservation per non-empty bin)
+// sm.cnt (records per bin) -> sm.sg.x (exclusive scan of the padded run
+// lengths) and sm.sg.y (one global reservation per non-empty bin)
 template <bool kBulk>
 __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem& sm) {
   constexpr int NW = kBThreads / 32;
@@ -404,8 +403,7 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
   for (int k = 0; k < 2; ++k) {
     const uint32_t r = lo + k;
     if (r < hi) {
-      sm.start[r] = run;
-      sm.gbase[r] = gb[k];
+      sm.sg[r] = make_uint2(run, gb[k]);
       if (kBulk && (sm.cnt[r] & 1u)) sm.rec[run + sm.cnt[r]] = kFiller;
       run += c[k];
     }
@@ -414,10 +412,11 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
 
 template <bool kBulk>
 __device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc, uint64_t cap) {
-  const uint32_t p = sm.start[b] + rank;
+  const uint2 sg = sm.sg[b];
+  const uint32_t p = sg.x + rank;
   sm.rec[p] = rc;
   if (!kBulk) {  // slot in the bin array (bin * cap + offset < 2^32), or none: bin full
-    const uint32_t o = sm.gbase[b] + rank;
+    const uint32_t o = sg.y + rank;
     sm.dst[p] = o < cap ? b * (uint32_t)cap + o : 0xFFFFFFFFu;
   }
 }
@@ -439,7 +438,7 @@ __device__ __forceinline__ void bin_write_coalesced(uint32_t nb, uint32_t total,
       uint32_t lo = 0, hi = nb - 1;
       while (lo < hi) {
         const uint32_t mid = (lo + hi + 1) >> 1;
-        if (sm.start[mid] <= p) lo = mid;
+        if (sm.sg[mid].x <= p) lo = mid;
         else hi = mid - 1;
       }
       ovf(rc, lo);
@@ -460,7 +459,7 @@ __device__ __forceinline__ void bin_write(uint32_t nb, uint64_t* __restrict__ ou
   for (uint32_t r = threadIdx.x; r < nb; r += kBThreads) {
     const uint32_t c = sm.cnt[r];
     if (!c) continue;
-    const uint32_t cr = (c + 1u) & ~1u, st = sm.start[r], gb = sm.gbase[r];
+    const uint32_t cr = (c + 1u) & ~1u, st = sm.sg[r].x, gb = sm.sg[r].y;
     uint64_t* dst = out + (uint64_t)r * cap;
     if ((uint64_t)gb + cr <= cap) {
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + gb),
