@@ -658,9 +658,9 @@ __global__ void __launch_bounds__(kBThreads, 3)
 constexpr int kPWarps = 30;                     // consumer warps
 constexpr int kPConsumers = kPWarps * 32;
 constexpr int kPThreads = kPConsumers + 32;     // + one producer warp (<= 1024 threads)
-constexpr int kPPerLane = 4;                    // records per consumer lane per chunk
-constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (3840)
-constexpr int kPStages = 3;
+constexpr int kPPerLane = 2;                    // records per consumer lane per chunk
+constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (1920)
+constexpr int kPStages = 6;
 template <int WPB>
 constexpr int kPSub = (8 / WPB) < kPPerLane ? (8 / WPB) : kPPerLane;  // records in flight per lane
 constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + 128;
