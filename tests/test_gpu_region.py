@@ -122,3 +122,25 @@ def test_region_delete_absent_keys_report_false():
     assert abs(int(got.sum()) - int(want.sum())) <= 2
     assert int(got.sum()) < 200
     assert len(filt) == len(keys) - int(got.sum())
+
+
+@pytest.mark.parametrize("pol", ["xor", "offset"])
+def test_l2_tiled_schedule_still_exact(monkeypatch, pol):
+    """CKF_SCHED=l2 selects the round-1 L2-tiled schedule (kept for comparison)."""
+    monkeypatch.setenv("CKF_SCHED", "l2")
+    cfg = _cfg(16, 16, pol, m=1 << 12)
+    rng = np.random.default_rng(21)
+    keys = rng.integers(0, 1 << 62, size=int(0.95 * cfg.total_slots), dtype=np.uint64)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    rok, _, _ = ref.insert_batch(keys)
+    filt = CuckooFilter(cfg, tiled=True)
+    l0 = _lib.kernel_launches()
+    res = filt.insert_batch(keys)
+    assert _lib.kernel_launches() - l0 >= 4  # bin, probe1, probe2, evict
+    assert res.n_failed == int((~rok).sum())
+    neg = rng.integers(1 << 62, 1 << 63, size=100_000, dtype=np.uint64)
+    assert filt.query_batch(keys).all()
+    snap = oracle.OracleFilter(oracle.cfg_from(cfg))
+    snap.words[:] = filt.words
+    assert np.array_equal(filt.query_batch(neg), snap.query_batch(neg))
+    assert filt.delete_batch(keys).all() and len(filt) == 0
