@@ -5,19 +5,23 @@
 // Table layout: uint64 words[m * wpb], bucket i = words
 // [i*wpb, (i+1)*wpb), lane s of a word = bits [s*f, (s+1)*f), 0 = empty
 // (reference filter.py:130, wordops.py:1-16).  With f=16, b=16 a bucket is one
-// 32-byte sector and is fetched by one 256-bit load.
+// 32-byte sector.
 //
-// Kernel families (all one thread per key, grid-stride over the batch):
-//   query_kernel   <F,WPB,POL,KPT>  read-only, 256-bit ld.global.nc bucket loads,
-//                                   KPT keys per thread for memory-level parallelism
-//   insert_kernel  <F,WPB,POL>      direct TryInsert into i1 then i2 with a 64-bit
-//                                   atomicCAS commit; keys whose pair is full are
-//                                   queued (warp-aggregated) for...
-//   evict_kernel   <F,POL>          ...the DFS / BFS eviction pass (K:374-436)
-//   delete_kernel  <F,WPB,POL>      TryRemove with CAS-clear (K:461-484)
-//   seq_*_kernel   <F,POL>          one device thread walking the batch in order:
-//                                   bit-identical to the reference insert_batch /
-//                                   delete_batch with workers=1 (parity mode)
+// Schedules, chosen per call (choose() below):
+//   region (ckf_region.cuh)  large batches on large tables: bin -> split ->
+//                            shared-memory probe per table region, twice
+//                            (primary, then alternate buckets), + eviction;
+//   L2-tiled (ckf_tiled.cuh) round-1 schedule, CKF_SCHED=l2 (comparison);
+//   direct (this file)       one thread per key:
+//     query_kernel   <F,WPB,POL,KPT>  read-only 256-bit bucket loads
+//     insert_kernel  <F,WPB,POL>      TryInsert i1 then i2 with a 64-bit
+//                                     atomicCAS; full pairs are queued for...
+//     evict_kernel   <F,WPB,POL>      ...the DFS / BFS eviction pass (K:374-436),
+//                                     also the last pass of the other schedules
+//     delete_kernel  <F,WPB,POL>      TryRemove with CAS-clear (K:461-484)
+//   sequential (parity mode)  seq_*_kernel: one device thread walking the batch
+//                            in order, bit-identical to the reference
+//                            insert_batch / delete_batch with workers=1.
 // WPB = words per bucket as a template constant for 1/2/4/8, or 0 for the
 // runtime-wpb generic path (any legal b).
 #include <cuda_runtime.h>
