@@ -637,11 +637,11 @@ __global__ void __launch_bounds__(kBThreads, 3)
 // probe: one persistent CTA per SM, fine regions resident in shared memory
 // ---------------------------------------------------------------------------
 
-constexpr int kPWarps = 30;                     // consumer warps
+constexpr int kPWarps = 24;                     // consumer warps (measured: 16 and 30 slower)
 constexpr int kPConsumers = kPWarps * 32;
 constexpr int kPThreads = kPConsumers + 32;     // + one producer warp (<= 1024 threads)
 constexpr int kPPerLane = 2;                    // records per consumer lane per chunk
-constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (1920)
+constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (1536)
 constexpr int kPStages = 6;
 template <int WPB>
 constexpr int kPSub = (8 / WPB) < kPPerLane ? (8 / WPB) : kPPerLane;  // records in flight per lane
