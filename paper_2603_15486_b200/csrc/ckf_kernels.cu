@@ -1002,7 +1002,7 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
   if (!ws || !tiled_applies(p, n, flags)) return t;
   t.ws = ws;
   bool ok = false;
-  if (use_region() && ((uintptr_t)keys % 16) == 0) {
+  if (use_region() && ((uintptr_t)keys % 8) == 0) {
     t.rpl = make_rplan(p, n, op, flags, ok);
     if (ok) {
       t.RL = rlayout_for(t.rpl, n, op);

@@ -482,13 +482,16 @@ __global__ void __launch_bounds__(kBThreads, 3)
   const uint64_t pol = evict_first_policy();
   const uint32_t lmask = (1u << pl.lrbc) - 1u;
   const uint64_t n = SRC == SRC_KEYS ? n_keys : w.n_miss[blockIdx.y];
+  const bool al16 = ((uintptr_t)keys & 15) == 0;  // 256-bit pair loads need 16 B alignment
   const uint4* ms = w.miss + (uint64_t)blockIdx.y * w.seg;
   uint32_t n_ok = 0, n_alt = 0;
   for (uint64_t t0 = blockIdx.x * KT; t0 < n; t0 += (uint64_t)gridDim.x * KT) {
     if (threadIdx.x == 0) {
       const uint64_t nx = t0 + (uint64_t)gridDim.x * KT;
-      if (nx < n && n - nx >= 2) {
-        if (SRC == SRC_KEYS) prefetch_l2(keys + nx, (uint32_t)(min((uint64_t)KT, n - nx) * 8) & ~15u);
+      if (SRC == SRC_KEYS && nx < n && n - nx >= 4) {  // 16 B-aligned window inside the next tile
+        const uintptr_t lo = ((uintptr_t)(keys + nx) + 15) & ~(uintptr_t)15;
+        const uintptr_t hi = (uintptr_t)(keys + nx + min(KT, n - nx)) & ~(uintptr_t)15;
+        if (hi > lo) prefetch_l2((const void*)lo, (uint32_t)(hi - lo));
       }
     }
     bin_release();
@@ -502,13 +505,13 @@ __global__ void __launch_bounds__(kBThreads, 3)
         const uint64_t i = t0 + (uint64_t)q * 2 * kBThreads + 2 * threadIdx.x;
         if (dual && q >= kBItems / 4) {
           kk[2 * q] = kk[2 * q + 1] = 0;
-        } else if (i + 1 < n) {
+        } else if (i + 1 < n && al16) {
           asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                        : "=l"(kk[2 * q]), "=l"(kk[2 * q + 1])
                        : "l"(keys + i), "l"(pol));
-        } else {
+        } else {  // tail, or keys only 8 B-aligned (a slice at an odd offset)
           kk[2 * q] = i < n ? keys[i] : 0;
-          kk[2 * q + 1] = 0;
+          kk[2 * q + 1] = i + 1 < n ? keys[i + 1] : 0;
         }
       }
       __syncthreads();

@@ -144,3 +144,25 @@ def test_l2_tiled_schedule_still_exact(monkeypatch, pol):
     snap.words[:] = filt.words
     assert np.array_equal(filt.query_batch(neg), snap.query_batch(neg))
     assert filt.delete_batch(keys).all() and len(filt) == 0
+
+
+def test_region_schedule_on_odd_offset_slices():
+    """A torch slice starting at an odd element is only 8 B-aligned: the region
+    schedule still runs (scalar key loads) and matches the oracle."""
+    cfg = _cfg(16, 16, "xor", m=1 << 12)
+    rng = np.random.default_rng(31)
+    host = rng.integers(0, 1 << 62, size=int(0.95 * cfg.total_slots) + 1, dtype=np.uint64)
+    keys = torch.from_numpy(host.view(np.int64)).cuda()[1:]
+    assert keys.data_ptr() % 16 == 8
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    rok, _, _ = ref.insert_batch(host[1:])
+    filt = CuckooFilter(cfg, tiled=True)
+    l0 = _lib.kernel_launches()
+    res = filt.insert_batch(keys)
+    assert _lib.kernel_launches() - l0 >= 7  # bin, split, probe, bin, split, probe, evict
+    assert res.n_failed == int((~rok).sum())
+    q = torch.from_numpy(np.concatenate([[0], host[1:2000], rng.integers(1 << 62, 1 << 63, 3001, dtype=np.uint64)]).view(np.int64)).cuda()[1:]
+    snap = oracle.OracleFilter(oracle.cfg_from(cfg))
+    snap.words[:] = filt.words
+    assert np.array_equal(filt.query_batch(q).cpu().numpy(), snap.query_batch(q.cpu().numpy().view(np.uint64)))
+    assert bool(filt.delete_batch(keys).all()) and len(filt) == 0
