@@ -148,6 +148,16 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                uint8_t* out, ckf_counters* counters, long long* occupancy, void* workspace,
                uint64_t workspace_bytes, unsigned flags, void* stream);
 
+/* Multi-GPU routing (sharded.py steps 2-3): stable partition of key hashes
+ * by owning shard (h >> shift) & (shards - 1), shards a power of two <= 8.
+ * send[] receives the hashes grouped by shard in arrival order, order[p] the
+ * source index of send[p], shard_counts[s] (device int64) the group sizes.
+ * workspace: ckf_route_workspace_bytes(n, shards) device bytes. */
+uint64_t ckf_route_workspace_bytes(uint64_t n, uint32_t shards);
+int ckf_route_partition(const uint64_t* hashes, uint64_t n, uint32_t shift, uint32_t shards, uint64_t* send,
+                        long long* order, long long* shard_counts, void* workspace, uint64_t workspace_bytes,
+                        void* stream);
+
 /* k-mer ingestion (replaces swarcuckoo/kmer.py:48-95 stream_kmers' packing
  * loop).  seq: device bytes of the FASTA records' sequence lines, each record's
  * lines concatenated, one separator byte (any byte outside ACGTacgt) between

@@ -79,6 +79,8 @@ SIGNATURES = {
     "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.c_uint, _vp]),
     "ckf_delete": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, ctypes.c_uint,
                                   _vp]),
+    "ckf_route_workspace_bytes": (_u64, [_u64, _u32]),
+    "ckf_route_partition": (ctypes.c_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp, _u64, _vp]),
     "ckf_kmer_workspace_bytes": (_u64, [_u64]),
     "ckf_kmers": (ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _u64, _vp]),
     "ckf_host_hash": (_u64, [_u64, _u64]),

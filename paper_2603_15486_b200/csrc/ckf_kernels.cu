@@ -835,6 +835,182 @@ static bool params_ok(const ckf_params* p) {
 }  // namespace ckf
 
 // ---------------------------------------------------------------------------
+// multi-GPU routing: stable partition of key hashes by owning shard
+// ---------------------------------------------------------------------------
+//
+// shard(h) = (h >> shift) & (G - 1), G <= 8 (one node).  Stable: shard s's
+// hashes leave in arrival order, so each shard sees exactly the key stream a
+// reference filter of m/G buckets would (sharded.py).  Three passes over
+// 4096-hash tiles (thread t owns 16 consecutive hashes of its tile): count per
+// (tile, shard), one-block scan to (tile, shard) offsets, scatter.  order[p] =
+// source index of send[p] (the return path's inverse permutation).
+
+constexpr int kRtThreads = 256, kRtItems = 16, kRtTile = kRtThreads * kRtItems;
+
+__global__ void __launch_bounds__(kRtThreads) route_count_kernel(const uint64_t* __restrict__ h, uint64_t n,
+                                                                 uint32_t shift, uint32_t gmask,
+                                                                 uint32_t* __restrict__ tile_counts) {
+  __shared__ uint32_t s_cnt[8];
+  if (threadIdx.x < 8) s_cnt[threadIdx.x] = 0;
+  __syncthreads();
+  uint64_t c = 0;  // counts only: coalesced strided items (order does not matter here)
+#pragma unroll
+  for (int k = 0; k < kRtItems; ++k) {
+    const uint64_t i = blockIdx.x * (uint64_t)kRtTile + k * kRtThreads + threadIdx.x;
+    if (i < n) c += 1ull << (8 * ((h[i] >> shift) & gmask));
+  }
+#pragma unroll
+  for (int s = 0; s < 8; ++s) {
+    const uint32_t v = __reduce_add_sync(0xffffffffu, (uint32_t)(c >> (8 * s)) & 0xFFu);
+    if ((threadIdx.x & 31) == 0 && v) atomicAdd(&s_cnt[s], v);
+  }
+  __syncthreads();
+  if (threadIdx.x <= gmask) tile_counts[blockIdx.x * (uint64_t)(gmask + 1) + threadIdx.x] = s_cnt[threadIdx.x];
+}
+
+// one block: offs[t * G + s] = base[s] + sum_{t' < t} counts[t' * G + s];
+// shard_counts[s] = total of s.  Shards are scanned one after the other.
+__global__ void __launch_bounds__(1024) route_scan_kernel(const uint32_t* __restrict__ tile_counts, uint64_t ntiles,
+                                                          uint32_t G, uint64_t* __restrict__ offs,
+                                                          long long* __restrict__ shard_counts) {
+  __shared__ uint64_t wprefix[32];
+  __shared__ uint64_t s_total, s_base;
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x / 32;
+  const uint64_t per = (ntiles + blockDim.x - 1) / blockDim.x;
+  const uint64_t lo = min((uint64_t)tid * per, ntiles), hi = min(lo + per, ntiles);
+  if (tid == 0) s_base = 0;
+  for (uint32_t s = 0; s < G; ++s) {
+    uint64_t sum = 0;
+    for (uint64_t t = lo; t < hi; ++t) sum += tile_counts[t * G + s];
+    uint64_t x = sum;  // inclusive warp scan
+#pragma unroll
+    for (int d = 1; d < 32; d <<= 1) {
+      const uint64_t y = __shfl_up_sync(0xffffffffu, x, d);
+      if (lane >= d) x += y;
+    }
+    __syncthreads();
+    if (lane == 31) wprefix[wid] = x;
+    __syncthreads();
+    if (wid == 0) {
+      const uint64_t v = lane < nw ? wprefix[lane] : 0;
+      uint64_t t = v;
+#pragma unroll
+      for (int d = 1; d < 32; d <<= 1) {
+        const uint64_t y = __shfl_up_sync(0xffffffffu, t, d);
+        if (lane >= d) t += y;
+      }
+      if (lane < nw) wprefix[lane] = t - v;
+      if (lane == 31) s_total = t;
+    }
+    __syncthreads();
+    uint64_t run = s_base + wprefix[wid] + x - sum;
+    for (uint64_t t = lo; t < hi; ++t) {
+      offs[t * G + s] = run;
+      run += tile_counts[t * G + s];
+    }
+    __syncthreads();
+    if (tid == 0) {
+      shard_counts[s] = (long long)s_total;
+      s_base += s_total;
+    }
+  }
+}
+
+// Scatter, staged through shared memory so every shard's run leaves as
+// coalesced stores: the tile is loaded coalesced (padded: thread t's 16
+// hashes start 17 words apart, no bank conflicts), each hash is placed at its
+// stable position inside the tile's shard-sorted layout, then the runs are
+// copied out.
+constexpr int kRtPad = kRtTile + kRtTile / kRtItems;  // one pad word per 16
+constexpr uint32_t kRouteSmem = (uint32_t)(kRtPad * 8 + kRtTile * 8 + kRtTile * 8);
+
+__global__ void __launch_bounds__(kRtThreads, 2) route_scatter_kernel(const uint64_t* __restrict__ h, uint64_t n,
+                                                                      uint32_t shift, uint32_t gmask,
+                                                                      const uint64_t* __restrict__ offs,
+                                                                      uint64_t* __restrict__ send,
+                                                                      long long* __restrict__ order) {
+  extern __shared__ __align__(16) uint64_t rsm[];
+  uint64_t* hin = rsm;                          // [kRtPad] tile, padded
+  uint64_t* hout = rsm + kRtPad;                // [kRtTile] shard-sorted hashes
+  long long* oout = (long long*)(hout + kRtTile);  // [kRtTile] their source indices
+  __shared__ uint64_t s_w[2][kRtThreads / 32];
+  __shared__ uint32_t s_start[9];
+  const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+  const uint64_t t0 = blockIdx.x * (uint64_t)kRtTile;
+  const uint32_t tn = (uint32_t)min((uint64_t)kRtTile, n - t0);
+  for (uint32_t j = tid; j < tn; j += kRtThreads) hin[j + j / kRtItems] = h[t0 + j];
+  __syncthreads();
+  uint8_t sh[kRtItems];
+  uint64_t c8 = 0;
+#pragma unroll
+  for (int k = 0; k < kRtItems; ++k) {
+    const uint32_t j = tid * kRtItems + k;
+    sh[k] = j < tn ? (uint8_t)((hin[j + j / kRtItems] >> shift) & gmask) : 0xFF;
+    if (sh[k] != 0xFF) c8 += 1ull << (8 * sh[k]);
+  }
+  uint64_t c0 = 0, c1 = 0;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    c0 |= ((c8 >> (8 * q)) & 0xFFull) << (16 * q);
+    c1 |= ((c8 >> (8 * (q + 4))) & 0xFFull) << (16 * q);
+  }
+  uint64_t x0 = c0, x1 = c1;
+#pragma unroll
+  for (int d = 1; d < 32; d <<= 1) {
+    const uint64_t y0 = __shfl_up_sync(0xffffffffu, x0, d), y1 = __shfl_up_sync(0xffffffffu, x1, d);
+    if (lane >= d) {
+      x0 += y0;
+      x1 += y1;
+    }
+  }
+  if (lane == 31) {
+    s_w[0][wid] = x0;
+    s_w[1][wid] = x1;
+  }
+  __syncthreads();
+  uint64_t p0 = x0 - c0, p1 = x1 - c1, t0s = 0, t1s = 0;  // my prefix; tile totals
+#pragma unroll
+  for (int k = 0; k < kRtThreads / 32; ++k) {
+    if (k < wid) {
+      p0 += s_w[0][k];
+      p1 += s_w[1][k];
+    }
+    t0s += s_w[0][k];
+    t1s += s_w[1][k];
+  }
+  uint32_t start[9];  // shard runs inside the tile's sorted layout
+  start[0] = 0;
+#pragma unroll
+  for (int q = 0; q < 8; ++q) start[q + 1] = start[q] + ((uint32_t)((q < 4 ? t0s : t1s) >> (16 * (q & 3))) & 0xFFFFu);
+  if (tid < 9) s_start[tid] = start[tid];
+  uint32_t next[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) next[q] = start[q] + ((uint32_t)((q < 4 ? p0 : p1) >> (16 * (q & 3))) & 0xFFFFu);
+#pragma unroll
+  for (int k = 0; k < kRtItems; ++k) {
+    if (sh[k] == 0xFF) continue;
+    uint32_t r = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q)
+      if (sh[k] == q) r = next[q]++;
+    const uint32_t j = tid * kRtItems + k;
+    hout[r] = hin[j + j / kRtItems];
+    oout[r] = (long long)(t0 + j);
+  }
+  __syncthreads();
+  const uint64_t* tb = offs + blockIdx.x * (uint64_t)(gmask + 1);
+  for (uint32_t p = tid; p < tn; p += kRtThreads) {
+    uint32_t q = 0;
+#pragma unroll
+    for (int k = 1; k < 8; ++k)
+      if (p >= s_start[k]) q = k;
+    const uint64_t pos = tb[q] + (p - s_start[q]);
+    send[pos] = hout[p];
+    order[pos] = oout[p];
+  }
+}
+
+// ---------------------------------------------------------------------------
 // k-mer ingestion (reference kmer.py:48-95)
 // ---------------------------------------------------------------------------
 //
@@ -1067,6 +1243,34 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,
                (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, keys, workspace, workspace_bytes)};
   return dispatch3<DeleteOp>(p, words, a);
+}
+
+uint64_t ckf_route_workspace_bytes(uint64_t n, uint32_t shards) {
+  const uint64_t nt = (n + kRtTile - 1) / kRtTile;
+  return align256(nt * shards * 4) + align256(nt * shards * 8);
+}
+
+int ckf_route_partition(const uint64_t* hashes, uint64_t n, uint32_t shift, uint32_t shards, uint64_t* send,
+                        long long* order, long long* shard_counts, void* workspace, uint64_t workspace_bytes,
+                        void* stream) {
+  if (shards < 1 || shards > 8 || (shards & (shards - 1)) || shift > 63 || !shard_counts) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (n == 0) return cudaMemsetAsync(shard_counts, 0, 8ull * shards, s) == cudaSuccess ? CKF_OK : cuda_error();
+  if (!hashes || !send || !order || !workspace || workspace_bytes < ckf_route_workspace_bytes(n, shards))
+    return CKF_EINVAL;
+  const uint64_t nt = (n + kRtTile - 1) / kRtTile;
+  if (nt > 0x7FFFFFFFull) return CKF_EINVAL;
+  uint32_t* counts = (uint32_t*)workspace;
+  uint64_t* offs = (uint64_t*)((char*)workspace + align256(nt * shards * 4));
+  const uint32_t gmask = shards - 1;
+  route_count_kernel<<<(unsigned)nt, kRtThreads, 0, s>>>(hashes, n, shift, gmask, counts);
+  int st = status();
+  if (st) return st;
+  route_scan_kernel<<<1, 1024, 0, s>>>(counts, nt, shards, offs, shard_counts);
+  if ((st = status())) return st;
+  allow_big_smem<route_scatter_kernel>(kRouteSmem);
+  route_scatter_kernel<<<(unsigned)nt, kRtThreads, kRouteSmem, s>>>(hashes, n, shift, gmask, offs, send, order);
+  return status();
 }
 
 uint64_t ckf_kmer_workspace_bytes(uint64_t len) {

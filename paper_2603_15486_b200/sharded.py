@@ -9,7 +9,8 @@ in arrival order.
 
 Per batch, on every rank (one process per GPU, NCCL over NVLink/NVSwitch):
   1. hash the local keys (ckf_hash kernel);
-  2. shard id per hash, stable permutation by shard, per-shard counts;
+  2. shard id per hash, stable permutation by shard, per-shard counts
+     (ckf_route_partition: count / scan / scatter kernels);
   3. all-to-all of the counts, then of the 8-byte hashes;
   4. the owning rank runs the local kernel on hashes (CKF_INPUT_HASHED:
      no rehash);
@@ -136,16 +137,37 @@ class ShardedCuckooFilter:
         h = self._hash(self._keys(keys))
         if self.world == 1:
             return h, None, None, None
-        shard = self.router.shard_of(h)
-        order = torch.argsort(shard, stable=True)
-        send = h[order]
-        send_counts = torch.bincount(shard, minlength=self.world)
+        if h.is_cuda:
+            send, order, send_counts = self._partition_cuda(h)
+        else:  # CPU stand-ins of the gloo tests
+            shard = self.router.shard_of(h).to(torch.uint8)
+            order = torch.argsort(shard, stable=True)
+            send = h[order]
+            send_counts = torch.bincount(shard, minlength=self.world)
         recv_counts = torch.empty_like(send_counts)
         dist.all_to_all_single(recv_counts, send_counts, group=self.group)
         sc, rc = send_counts.tolist(), recv_counts.tolist()
         recv = torch.empty(sum(rc), dtype=h.dtype, device=h.device)
         dist.all_to_all_single(recv, send, rc, sc, group=self.group)
         return recv, order, sc, rc
+
+    def _partition_cuda(self, h: torch.Tensor):
+        """Stable partition by shard on the device (ckf_route_partition: count,
+        scan, scatter -- a torch stable argsort of 2^28 ids takes ~24 ms)."""
+        from . import _lib
+
+        L = _lib.lib()
+        n = h.numel()
+        send = torch.empty_like(h)
+        order = torch.empty(n, dtype=torch.int64, device=h.device)
+        counts = torch.empty(self.world, dtype=torch.int64, device=h.device)
+        wsb = int(L.ckf_route_workspace_bytes(n, self.world))
+        if getattr(self, "_route_ws", None) is None or self._route_ws.numel() < wsb:
+            self._route_ws = torch.empty(max(wsb, 1), dtype=torch.uint8, device=h.device)
+        _lib.check(L.ckf_route_partition(h.data_ptr(), n, self.router.shift, self.world, send.data_ptr(),
+                                         order.data_ptr(), counts.data_ptr(), self._route_ws.data_ptr(), wsb,
+                                         torch.cuda.current_stream(h.device).cuda_stream))
+        return send, order, counts
 
     def _gather(self, local_res: torch.Tensor, order, sc, rc) -> torch.Tensor:
         """Steps 5-6: answers back to their source rank, then to caller order."""
