@@ -643,11 +643,11 @@ __global__ void __launch_bounds__(kBThreads, 3)
 constexpr int kPWarps = 24;                     // consumer warps (measured: 16 and 30 slower)
 constexpr int kPConsumers = kPWarps * 32;
 constexpr int kPThreads = kPConsumers + 32;     // + one producer warp (<= 1024 threads)
-constexpr int kPPerLane = 2;                    // records per consumer lane per chunk
-constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (1536)
-constexpr int kPStages = 6;
+constexpr int kPPerLane = 4;                    // records per consumer lane per chunk
+constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (3072)
+constexpr int kPStages = 3;
 template <int WPB>
-constexpr int kPSub = (8 / WPB) < kPPerLane ? (8 / WPB) : kPPerLane;  // records in flight per lane
+constexpr int kPSub = (16 / WPB) < kPPerLane ? (16 / WPB) : kPPerLane;  // records in flight per lane
 constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + 128;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
