@@ -4,7 +4,7 @@
 # usage: tools/ncu_capture.sh <name> <kernel-regex> <skip> -- <command...>
 set -u
 name=$1; regex=$2; skip=$3; shift 4
-ncu --set full --import-source on --clock-control none -k "regex:$regex" -s "$skip" -c 1 \
+ncu -f --set full --import-source on --clock-control none -k "regex:$regex" -s "$skip" -c 1 \
     -o "/tmp/$name" "$@" > "gpurun_out/$name.log" 2>&1
 for page in details raw source; do
   ncu -i "/tmp/$name.ncu-rep" --page $page --csv > "gpurun_out/${name}_$page.csv" 2>/dev/null
