@@ -347,9 +347,7 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
 #define CKF_CASE_P(FF)                                        \
   if (p->policy == CKF_POLICY_XOR) { CKF_CASE_W(FF, 0) }      \
   else { CKF_CASE_W(FF, 1) }
-#if defined(CKF_DEV_MIN)  // developer build: the bench configuration only (f=16, b=16, xor)
-  if (p->fingerprint_bits == 16 && p->policy == CKF_POLICY_XOR && vec == 4) return Op<16, 4, 0>::run(a...);
-#elif defined(CKF_DEV_F16)  // developer build: f=16 only (fast compile)
+#ifdef CKF_DEV_F16  // developer build: f=16 only (fast compile)
   if (p->fingerprint_bits == 16) { CKF_CASE_P(16) }
 #else
   switch (p->fingerprint_bits) {
@@ -541,15 +539,11 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   pl.R = pl.R1 * pl.F2;
   pl.pb = pb;
   const double recs = (double)n * (op == CKF_OP_QUERY ? 2.0 : 1.0);  // dual query records
-  // coarse bins: one segment per stage CTA; + one filler-padded line at the end
-  pl.G1 = (uint32_t)sm_count();
-  pl.S = stage_slots(pl.R1);
-  const double per_seg = recs / ((double)pl.R1 * pl.G1);
-  pl.cap1 = ((uint64_t)(per_seg + 8.0 * std::sqrt(per_seg) + 64.0) + 2 * kSLine - 1) / kSLine * kSLine;
-  // fine bins: + run padding, at most one filler per fine bin per split tile
-  const uint64_t split_tiles =
-      (uint64_t)((pl.G1 + kSplitGroup - 1) / kSplitGroup) * ((kSplitGroup * pl.cap1 + kBTile - 1) / kBTile);
-  pl.capf = (even_cap(recs / pl.R) + split_tiles + 1) & ~1ull;
+  // + run padding: at most one filler per bin per tile of the pass that fills it
+  // (bin: ceil(n / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
+  const uint64_t tiles1 = (n + kBTile - 1) / kBTile + (uint64_t)kMaxProbeGrid;
+  pl.cap1 = (even_cap(recs / pl.R1) + tiles1 + 1) & ~1ull;
+  pl.capf = (even_cap(recs / pl.R) + (pl.cap1 + kBTile - 1) / kBTile + 1) & ~1ull;
   ok = true;
   return pl;
 }
@@ -571,13 +565,13 @@ static RLayout rlayout_for(const RPlan& pl, uint64_t n, int op) {
   RLayout L{};
   const uint64_t cs = (uint64_t)kCntStride * 4;
   L.cnt1 = 0;
-  L.cntf = align256(L.cnt1 + (uint64_t)pl.R1 * pl.G1 * 4);
+  L.cntf = align256(L.cnt1 + pl.R1 * cs);
   L.bin_ctr_end = align256(L.cntf + pl.R * cs);  // bin counters: zeroed again between the phases
   L.n_miss = L.bin_ctr_end;
   L.mode = L.n_miss + 4ull * kMaxProbeGrid;
   L.ctr_end = align256(L.mode + 8);
   L.bin1 = L.ctr_end;
-  L.binf = align256(L.bin1 + (uint64_t)pl.R1 * pl.G1 * pl.cap1 * 8);
+  L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
   L.miss = align256(L.binf + pl.R * pl.capf * 8);
   L.bits = align256(L.miss + probe_grid(pl) * miss_seg(pl) * 16);
   L.total = align256(L.bits + (op == CKF_OP_INSERT ? 0 : (n + 31) / 32 * 4));
@@ -638,16 +632,16 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   long long* mocc = OP == OP_QUERY ? nullptr : occ;
   const int sms = sm_count();
   const unsigned pg = probe_grid(pl);
-  const uint32_t kStSmem = stage_smem(pl.R1);
-  allow_big_smem<region_stage_kernel<OP, F, WPB, POL, SRC_KEYS>>(stage_smem(kRMaxCoarse));
-  allow_big_smem<region_stage_kernel<OP, F, WPB, POL, SRC_MISS>>(stage_smem(kRMaxCoarse));
+  constexpr uint32_t kBinSmem = sizeof(BinSmem);
+  allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
+  allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
   allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmemBulk);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmem);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
   int st;
   // phase 1: primary buckets
-  region_stage_kernel<OP, F, WPB, POL, SRC_KEYS><<<pl.G1, kSThreads, kStSmem, s>>>(g, pl, words, keys, n, hashed, w,
-                                                                                 sk, mocc, 0u);
+  region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, 3), kBThreads, kBinSmem, s>>>(
+      g, pl, words, keys, n, hashed, w, sk, mocc);
   if ((st = status())) return st;
   region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
@@ -655,8 +649,8 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   if ((st = status())) return st;
   // phase 2: the misses, on their alternate buckets
   if (cudaMemsetAsync(ws, 0, L.bin_ctr_end, s) != cudaSuccess) return cuda_error();
-  region_stage_kernel<OP, F, WPB, POL, SRC_MISS><<<pl.G1, kSThreads, kStSmem, s>>>(g, pl, words, keys, 0, hashed, w,
-                                                                                 sk, mocc, pg);
+  region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * 3 + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
+      g, pl, words, keys, 0, hashed, w, sk, mocc);
   if ((st = status())) return st;
   region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;

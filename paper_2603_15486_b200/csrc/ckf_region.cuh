@@ -262,9 +262,7 @@ constexpr int kRMaxCoarse = 512;
 // Record (8 B): index:32 | alt:1 | bucket offset in its region << pb | fp.
 // `alt` marks a record of the key's alternate bucket.
 struct RPlan {
-  uint64_t cap1;     // record slots per coarse-bin SEGMENT (a multiple of 16)
-  uint32_t G1;       // segments per coarse bin (= stage CTAs: segment (b, c) is written by CTA c only)
-  uint32_t S;        // staging slots per coarse bin in a stage CTA
+  uint64_t cap1;     // record slots per coarse bin (even)
   uint64_t capf;     // record slots per fine bin (even)
   uint32_t R1;       // coarse bins
   uint32_t lrbc;     // log2 buckets per coarse region
@@ -279,7 +277,7 @@ __device__ __forceinline__ uint64_t rpack(uint64_t idx, uint32_t alt, uint64_t o
 }
 
 struct RWork {
-  uint32_t* cnt1;   // [R1 * G1] coarse bin segment fill (records incl. line padding)
+  uint32_t* cnt1;   // [R1 * kCntStride] coarse bin fill
   uint32_t* cntf;   // [R * kCntStride] fine bin fill
   uint64_t* bin1;   // [R1 * cap1] coarse bins
   uint64_t* binf;   // [R * capf] fine bins
@@ -576,254 +574,6 @@ __global__ void __launch_bounds__(kBThreads, 3)
 }
 
 // ---------------------------------------------------------------------------
-// stage: hash + placement, binned by coarse region through shared-memory
-// staging lines (the round-2 bin pass)
-// ---------------------------------------------------------------------------
-//
-// Measured on B200 (tools/probe_bin.cu, profiles/r02_probe_bin.txt): the L2
-// accepts ~35-40 G scattered store requests/s whatever their size up to a
-// sector, while hashing + a shared-memory counter per key runs at ~340 G
-// keys/s.  So a bin pass is bound by store REQUESTS, and records should
-// leave inside whole 128 B lines.  Each persistent CTA keeps, per coarse bin,
-// a ring of pl.S staging slots in shared memory.  A round = kSRound records:
-//   A   hash + place; rank within the round r = atomicAdd(round count of the
-//       bin); the first T = S - 16 arrivals are admitted at position
-//       count(bin) + r (the rest -- a Poisson tail, ~1e-6 per bin and round
-//       at R1 = 512 -- are resolved directly on the global table, legal here
-//       because no region is resident in shared memory while this runs); a
-//       record whose position ends a 16-record line appends the line to the
-//       round's flush list;
-//   B   (barrier) staged writes; per-bin count += min(round count, T);
-//   C   (barrier) every listed line leaves as one 128 B TMA bulk store into
-//       the CTA's PRIVATE segment of the bin (no global atomics: coarse bin b
-//       = pl.G1 segments of pl.cap1 records, segment (b, c) written by CTA c).
-// The ring never overflows: at most 15 unflushed + T admitted <= S slots.
-// Keys (or phase-2 miss entries) are loaded into registers one round ahead.
-
-constexpr int kSThreads = 1024;
-constexpr int kSItems = 2;                      // records per thread per round
-constexpr int kSRound = kSThreads * kSItems;    // 2048
-constexpr int kSLine = 16;                      // records per line (128 B)
-constexpr int kSList = kSRound / kSLine + 512;  // lines completing in one round: <= sum over bins of ceil(arrivals / 16)
-constexpr uint32_t kSNone = 0xFFFFFFFFu;
-constexpr int kSplitGroup = 16;                 // stage segments per split work item (a power of two)
-
-// staging slots per bin: a power of two >= 32, the ring in <= 128 KiB
-__host__ __device__ constexpr uint32_t stage_slots(uint32_t R1) {
-  uint32_t s = 32;
-  while (s < 2048 && (uint64_t)R1 * s * 2 * 8 <= 128u * 1024u) s <<= 1;
-  return s;
-}
-__host__ __device__ constexpr uint32_t stage_smem(uint32_t R1) {
-  return R1 * stage_slots(R1) * 8 + R1 * 8 + 2 * kSList * 4 + 16;
-}
-
-// Source rounds of one stage CTA: (segment y, first item t0), t0 advancing by
-// G * KPR within a source segment (SRC_KEYS: one segment, the batch).
-struct StageIter {
-  uint32_t y;
-  uint64_t t0;
-};
-
-template <int OP, int F, int WPB, int POL, int SRC>
-__global__ void __launch_bounds__(kSThreads, 1)
-    region_stage_kernel(Geo g, RPlan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n_keys,
-                        bool hashed, RWork w, Sink sk, long long* occ, uint32_t n_src_segs) {
-  extern __shared__ __align__(128) uint8_t ssm[];
-  constexpr uint32_t PB = POL == CKF_POLICY_OFFSET ? F - 1 : F;  // payload (record fp) bits
-  const uint32_t R1 = pl.R1, S = pl.S, SM = pl.S - 1u, T = pl.S - kSLine;
-  uint64_t* stg = reinterpret_cast<uint64_t*>(ssm);                        // [R1][S] staging rings
-  uint32_t* bcnt = reinterpret_cast<uint32_t*>(ssm + (size_t)R1 * S * 8);  // [R1] records admitted before this round
-  uint32_t* brc = bcnt + R1;                                                // [R1] arrivals in this round
-  uint32_t* list = brc + R1;                                                // [2][kSList] bin << 20 | line
-  uint32_t* s_nlist = list + 2 * kSList;                                    // [2]
-  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const uint32_t G = gridDim.x, c = blockIdx.x;
-  const uint32_t lrbc = pl.lrbc, lmask = (1u << pl.lrbc) - 1u;
-  const uint64_t cap = pl.cap1;
-  // dual: a query batch sampled as mostly negative gets an i1 AND an i2 record
-  // per key (no phase 2); a round then covers kSThreads keys
-  const bool dual = OP == OP_QUERY && SRC == SRC_KEYS && w.mode[0] == 0;
-  const uint32_t KPR = dual ? kSThreads : kSRound;  // source items per round
-  const bool al16 = ((uintptr_t)keys & 15) == 0;
-  const uint32_t nsegs = SRC == SRC_KEYS ? 1u : n_src_segs;
-  const uint64_t pol = evict_first_policy();
-  auto seg_n = [&](uint32_t y) -> uint64_t { return SRC == SRC_KEYS ? n_keys : w.n_miss[y]; };
-  auto next = [&](StageIter it) -> StageIter {
-    it.t0 += (uint64_t)G * KPR;
-    while (it.y < nsegs && it.t0 >= seg_n(it.y)) {
-      ++it.y;
-      it.t0 = (uint64_t)c * KPR;
-    }
-    return it;
-  };
-  // this thread's source items of round `it` (registers; prefetched a round ahead)
-  struct Src {
-    uint64_t a[2], b[2];
-  };
-  auto load = [&](StageIter it, Src& sv) {
-    sv.a[0] = sv.a[1] = sv.b[0] = sv.b[1] = 0;
-    if (it.y >= nsegs) return;
-    const uint64_t n = seg_n(it.y);
-    if constexpr (SRC == SRC_KEYS) {
-      if (dual) {
-        const uint64_t i = it.t0 + tid;
-        if (i < n) sv.a[0] = ld_stream_ef(keys + i, pol);
-      } else {
-        const uint64_t i = it.t0 + 2 * (uint64_t)tid;
-        if (i + 1 < n && al16) {
-          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
-                       : "=l"(sv.a[0]), "=l"(sv.a[1])
-                       : "l"(keys + i), "l"(pol));
-        } else {
-          if (i < n) sv.a[0] = keys[i];
-          if (i + 1 < n) sv.a[1] = keys[i + 1];
-        }
-      }
-    } else {
-      const uint4* ms = w.miss + (uint64_t)it.y * w.seg + it.t0 + 2 * (uint64_t)tid;
-      const uint64_t i = it.t0 + 2 * (uint64_t)tid;
-      if (i < n) {
-        const uint4 v = ms[0];
-        sv.a[0] = (uint64_t)v.x | ((uint64_t)v.y << 32);
-        sv.b[0] = (uint64_t)v.z | ((uint64_t)v.w << 32);
-      }
-      if (i + 1 < n) {
-        const uint4 v = ms[1];
-        sv.a[1] = (uint64_t)v.x | ((uint64_t)v.y << 32);
-        sv.b[1] = (uint64_t)v.z | ((uint64_t)v.w << 32);
-      }
-    }
-  };
-  for (uint32_t i = tid; i < R1; i += kSThreads) bcnt[i] = brc[i] = 0;
-  if (tid == 0) s_nlist[0] = s_nlist[1] = 0;
-  __syncthreads();
-  uint32_t n_ok = 0, n_alt = 0;
-  auto seg = [&](uint32_t b) -> uint64_t* { return w.bin1 + ((uint64_t)b * G + c) * cap; };
-  auto ovf = [&](uint64_t rc, uint32_t b) {
-    const uint64_t bucket = ((uint64_t)b << lrbc) + ((rc >> PB) & lmask);
-    resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
-  };
-  StageIter it{0u, (uint64_t)c * KPR};
-  while (it.y < nsegs && it.t0 >= seg_n(it.y)) {
-    ++it.y;
-    it.t0 = (uint64_t)c * KPR;
-  }
-  Src cur, nxt;
-  load(it, cur);
-  for (uint32_t k = 0; it.y < nsegs; ++k) {  // block-uniform
-    const uint64_t n = seg_n(it.y), t0 = it.t0;
-    const uint32_t par = k & 1u;
-    const StageIter in = next(it);
-    load(in, nxt);  // next round's items, in flight during this round
-    // ---- A: records, positions, completed lines ----
-    uint64_t rec[kSItems];
-    uint32_t bin[kSItems], pos[kSItems];
-#pragma unroll
-    for (int q = 0; q < kSItems; ++q) {
-      pos[q] = kSNone;
-      bin[q] = 0;
-      rec[q] = kFiller;
-    }
-#pragma unroll
-    for (int q = 0; q < kSItems; ++q) {
-      const uint32_t e = (SRC == SRC_KEYS && dual) ? (uint32_t)tid : 2u * tid + q;
-      const uint64_t i = t0 + e;
-      if (i >= n) continue;
-      uint32_t idx, fp, bk, alt;
-      if constexpr (SRC == SRC_KEYS) {
-        if (dual && q == 1) {  // the i2 record of the same key (from q = 0's record)
-          fp = (uint32_t)rec[0] & ((1u << PB) - 1u);
-          const uint64_t b1 = ((uint64_t)bin[0] << lrbc) + (((uint32_t)rec[0] >> PB) & lmask);
-          uint64_t cc;
-          bk = (uint32_t)alt_index<POL>(b1, fp, 0, g, cc);
-          alt = 1u;
-        } else {
-          const uint64_t h = hashed ? cur.a[q] : xxh64(cur.a[q], g.seed);
-          const uint32_t fp0 = (uint32_t)(h >> 32) & ((1u << PB) - 1u);
-          fp = fp0 ? fp0 : 1u;
-          bk = (uint32_t)reduce_index(h & 0xFFFFFFFFull, g);
-          alt = 0u;
-        }
-        idx = (uint32_t)i;
-      } else {
-        idx = (uint32_t)cur.a[q];
-        fp = (uint32_t)(cur.a[q] >> 32);
-        bk = (uint32_t)cur.b[q];  // (m <= 2^32: the alternate bucket fits 32 bits)
-        alt = 1u;
-      }
-      bin[q] = bk >> lrbc;
-      rec[q] = ((uint64_t)idx << 32) | (alt << 31) | ((bk & lmask) << PB) | fp;
-    }
-    cur = nxt;
-    it = in;
-    uint32_t ln[kSItems];  // completed line (bin << 20 | line) or kSNone
-#pragma unroll
-    for (int q = 0; q < kSItems; ++q) {
-      ln[q] = kSNone;
-      if (is_filler(rec[q])) continue;
-      const uint32_t r = atomicAdd(&brc[bin[q]], 1u);
-      const uint32_t p = bcnt[bin[q]] + r;
-      if (r < T && p < cap) {
-        pos[q] = p;
-        if ((p & (kSLine - 1)) == kSLine - 1) ln[q] = (bin[q] << 20) | (p / kSLine);
-      } else {
-        ovf(rec[q], bin[q]);  // a record over the round's admission (or a full segment): never staged
-        if (r < T) pos[q] = kSNone - 1u;  // admitted past the segment: its position is a hole line
-      }
-    }
-    {  // append completed lines: one shared reservation per warp
-      const unsigned bal0 = __ballot_sync(0xffffffffu, ln[0] != kSNone),
-                     bal1 = __ballot_sync(0xffffffffu, ln[1] != kSNone);
-      const uint32_t tot = __popc(bal0) + __popc(bal1);
-      if (tot) {
-        uint32_t base = 0;
-        if (lane == 0) base = atomicAdd(&s_nlist[par], tot);
-        base = __shfl_sync(0xffffffffu, base, 0);
-        const unsigned lt = (1u << lane) - 1u;
-        uint32_t o = base + __popc(bal0 & lt) + __popc(bal1 & lt);
-        if (ln[0] != kSNone) list[par * kSList + o++] = ln[0];
-        if (ln[1] != kSNone) list[par * kSList + o] = ln[1];
-      }
-    }
-    __syncthreads();  // B: positions taken; the previous round's flush has read the ring
-#pragma unroll
-    for (int q = 0; q < kSItems; ++q)
-      if (pos[q] < kSNone - 1u) stg[bin[q] * S + (pos[q] & SM)] = rec[q];
-    for (uint32_t b = tid; b < R1; b += kSThreads) {
-      const uint32_t r = brc[b];
-      if (r) {
-        bcnt[b] += min(r, T);
-        brc[b] = 0;
-      }
-    }
-    if (tid == 0) s_nlist[par ^ 1u] = 0;  // next round's list
-    __syncthreads();  // C: this round's records are staged
-    // ---- flush: one completed line per half-warp, one coalesced 128 B store ----
-    const uint32_t nl = s_nlist[par];
-    for (uint32_t e = warp * 2 + (lane >> 4); e < nl; e += (kSThreads / 32) * 2) {
-      const uint32_t ent = list[par * kSList + e], b = ent >> 20, h = ent & 0xFFFFFu;
-      const uint64_t v = stg[b * S + ((h * kSLine) & SM) + (lane & 15)];
-      st_stream_ef(seg(b) + (uint64_t)h * kSLine + (lane & 15), v, pol);
-    }
-  }
-  __syncthreads();
-  // final partial lines (filler-padded to a whole line) and segment counts
-  for (uint32_t b = tid; b < R1; b += kSThreads) {
-    const uint32_t cnt = bcnt[b];
-    const uint32_t h = cnt / kSLine, rem = cnt % kSLine;
-    if (rem && (uint64_t)h * kSLine < cap) {
-      uint64_t* d = seg(b) + (uint64_t)h * kSLine;
-      const uint64_t* sp = stg + b * S + ((h * kSLine) & SM);
-      for (uint32_t q = 0; q < (uint32_t)kSLine; ++q) d[q] = q < rem ? sp[q] : kFiller;
-    }
-    const uint64_t padded = ((uint64_t)cnt + kSLine - 1) / kSLine * kSLine;
-    w.cnt1[(uint64_t)b * G + c] = (uint32_t)(padded < cap ? padded : cap);
-  }
-  block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
-}
-
-// ---------------------------------------------------------------------------
 // split: coarse bin -> F2 fine bins (records re-based to the fine region)
 // ---------------------------------------------------------------------------
 
@@ -833,59 +583,42 @@ __global__ void __launch_bounds__(kBThreads, 3)
   extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
   BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
   const uint64_t pol = evict_first_policy();
-  // work item = (coarse bin c, a group of kSplitGroup stage segments); its
-  // records are walked as one stream in kBTile tiles across the segments
-  const uint32_t ngroups = (pl.G1 + kSplitGroup - 1) / kSplitGroup;
-  const uint64_t items = (uint64_t)pl.R1 * ngroups;
+  const uint32_t tiles_per_bin = (uint32_t)((pl.cap1 + kBTile - 1) / kBTile);
+  const uint64_t tiles = (uint64_t)pl.R1 * tiles_per_bin;
   const uint32_t fshift = pl.pb + pl.lrb;  // offset bits above the fine offset
   const uint32_t fmask = pl.F2 - 1u;
   const uint64_t keep = ~((uint64_t)((1u << (pl.lrbc - pl.lrb)) - 1u) << fshift);  // clears the fine-region bits
-  __shared__ uint32_t s_pref[kSplitGroup + 1];
   uint32_t n_ok = 0, n_alt = 0;
-  for (uint64_t item = blockIdx.x; item < items; item += gridDim.x) {
-    const uint32_t c = (uint32_t)(item / ngroups);
-    const uint32_t g0 = (uint32_t)(item % ngroups) * kSplitGroup;
-    const uint32_t gn = min((uint32_t)kSplitGroup, pl.G1 - g0);
-    const uint64_t sg0 = (uint64_t)c * pl.G1 + g0;  // first segment of the group
-    __syncthreads();  // s_pref of the previous item is consumed
-    if (threadIdx.x == 0) {
-      uint32_t run = 0;
-      for (uint32_t j = 0; j < gn; ++j) {
-        s_pref[j] = run;
-        const uint32_t cc = w.cnt1[sg0 + j];
-        run += cc < pl.cap1 ? cc : (uint32_t)pl.cap1;
-      }
-      for (uint32_t j = gn; j <= (uint32_t)kSplitGroup; ++j) s_pref[j] = run;
-    }
-    __syncthreads();
-    const uint32_t total = s_pref[kSplitGroup];
-    for (uint32_t off0 = 0; off0 < total; off0 += kBTile) {  // block-uniform
+  for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
+    const uint32_t c = (uint32_t)(s / tiles_per_bin);
+    const uint64_t off0 = (s % tiles_per_bin) * (uint64_t)kBTile;
+    const uint32_t cc = w.cnt1[(size_t)c * kCntStride];
+    const uint64_t cnt = cc < pl.cap1 ? cc : pl.cap1;
+    if (off0 >= cnt) continue;  // block-uniform
     bin_release();
     for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.cnt[r] = 0;
-    const uint32_t nrec = min((uint32_t)kBTile, total - off0);
-    // segment counts are whole 16-record lines, so a record pair never straddles
-    // two segments: thread t loads pairs t, t + kBThreads, ... (16 B each)
+    const uint64_t* src = w.bin1 + c * pl.cap1 + off0;
+    const uint32_t nrec = (uint32_t)min((uint64_t)kBTile, cnt - off0);
     uint64_t rec[kBItems];
-    uint32_t j = 0;  // the segment holding the current pair (positions only grow)
 #pragma unroll
     for (int q = 0; q < kBItems / 2; ++q) {
       const uint32_t e = q * 2 * kBThreads + 2 * threadIdx.x;
-      rec[2 * q] = rec[2 * q + 1] = kFiller;
-      if (e < nrec) {
-        const uint32_t p = off0 + e;
-        while (s_pref[j + 1] <= p) ++j;
-        const uint64_t* a = w.bin1 + (sg0 + j) * pl.cap1 + (p - s_pref[j]);
+      if (e + 1 < nrec) {
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                      : "=l"(rec[2 * q]), "=l"(rec[2 * q + 1])
-                     : "l"(a), "l"(pol));
+                     : "l"(src + e), "l"(pol));
+      } else {
+        rec[2 * q] = e < nrec ? src[e] : 0;
+        rec[2 * q + 1] = 0;
       }
     }
     __syncthreads();
     uint32_t pk[kBItems];
 #pragma unroll
     for (int q = 0; q < kBItems; ++q) {
+      const uint32_t e = (q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
       const uint32_t f = (uint32_t)(rec[q] >> fshift) & fmask;
-      pk[q] = !is_filler(rec[q]) ? (f << 16) | atomicAdd(&sm.cnt[f], 1u) : 0xFFFFFFFFu;
+      pk[q] = e < nrec && !is_filler(rec[q]) ? (f << 16) | atomicAdd(&sm.cnt[f], 1u) : 0xFFFFFFFFu;
     }
     __syncthreads();
     bin_reserve<true>(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
@@ -898,7 +631,6 @@ __global__ void __launch_bounds__(kBThreads, 3)
       resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
     });
     __syncthreads();
-    }
   }
   bulk_wait_all();
   block_count_add(n_ok, n_alt, sk.ctr, occ, OP == OP_DELETE ? -1 : +1);
