@@ -19,7 +19,8 @@ owning GPU with NCCL all-to-all (paper_2603_15486_b200/sharded.py).
 
 `--impl reference` times the reference algorithm on the host CPU cores (the
 C restatement in oracle/, the reference itself being a numba package that
-does not ship to the GPU box), on a bounded 2^24-slot sample per step.
+does not ship to the GPU box) on the same 2^28-slot table, a bounded 1/16
+sample of each op's keys per step (CpuArm).
 """
 
 from __future__ import annotations
@@ -115,31 +116,70 @@ class ClockSampler:
 # CPU reference arm (oracle/ = C restatement of swarcuckoo's kernels)
 # --------------------------------------------------------------------------
 
-def cpu_protocol(log2_slots: int, pos: np.ndarray, neg: np.ndarray, threads: int) -> dict:
-    """One pass of the step protocol on the CPU: insert (1 thread, like the
-    reference's fused workers=1 kernel), lookup+/- (`threads` threads, like its
-    nogil query workers), delete (1 thread)."""
-    import oracle
+CPU_SAMPLE = 16  # the CPU arm times 1/16 of each op's keys per step
 
-    cfg = oracle.make_cfg(1 << (log2_slots - 4), 16, 16, "xor", "bfs", 500, 0)
-    n = int(0.95 * (1 << log2_slots))
-    p, q = pos[:n], neg[:n]
-    filt = oracle.OracleFilter(cfg)
-    t0 = time.perf_counter()
-    ok, _, _ = filt.insert_batch(p)
-    t1 = time.perf_counter()
-    hp = filt.query_batch(p, threads=threads)
-    t2 = time.perf_counter()
-    hn = filt.query_batch(q, threads=threads)
-    t3 = time.perf_counter()
-    filt.delete_batch(p)
-    t4 = time.perf_counter()
-    assert ok.all() and hp.all() and filt.occupancy == 0
-    total = t4 - t0
-    return {"n": n, "seconds": total, "value": 4 * n / total / 1e9,
-            "per_op_Mops": {"insert": n / (t1 - t0) / 1e6, "lookup+": n / (t2 - t1) / 1e6,
-                            "lookup-": n / (t3 - t2) / 1e6, "delete": n / (t4 - t3) / 1e6},
-            "fpr": float(hn.mean())}
+
+def cpu_model() -> str:
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown CPU"
+
+
+class CpuArm:
+    """configs[1] on the host cores with the reference algorithm (oracle/ C port).
+
+    Table: the full 2^log2-slot f=16 b=16 xor/bfs filter.  Setup (untimed,
+    once): insert all but the last 1/CPU_SAMPLE of the n positive keys with
+    the reference's workers>1 mode (filter.py:422-438; oracle
+    ck_insert_batch_mt).  Step (a bounded sample of the step protocol on that
+    same table): insert the held-back sample (load ~89 % -> 95 %), lookup+ of
+    it, lookup- of as many negatives, delete it again (back to ~89 %); inserts
+    and deletes in `threads` concurrent workers, lookups on `threads` threads
+    (filter.py:458-469).  value = 4 * sample / step time."""
+
+    def __init__(self, log2_slots: int, pos: np.ndarray, neg: np.ndarray, threads: int):
+        import oracle
+
+        oracle.build()
+        self.threads = threads
+        self.log2 = log2_slots
+        cfg = oracle.make_cfg(1 << (log2_slots - 4), 16, 16, "xor", "bfs", 500, 0)
+        self.n = len(pos)
+        self.s = self.n // CPU_SAMPLE
+        self.filt = oracle.OracleFilter(cfg)
+        t0 = time.perf_counter()
+        ok = self.filt.insert_batch_mt(pos[: self.n - self.s], threads)
+        self.setup_s = time.perf_counter() - t0
+        assert ok.all()
+        self.p, self.q = pos[self.n - self.s:], neg[: self.s]
+
+    def step(self) -> dict:
+        f, s, th = self.filt, self.s, self.threads
+        t0 = time.perf_counter()
+        ok = f.insert_batch_mt(self.p, th)
+        t1 = time.perf_counter()
+        hp = f.query_batch(self.p, threads=th)
+        t2 = time.perf_counter()
+        hn = f.query_batch(self.q, threads=th)
+        t3 = time.perf_counter()
+        d = f.delete_batch_mt(self.p, th)
+        t4 = time.perf_counter()
+        assert ok.all() and hp.all() and d.all()
+        total = t4 - t0
+        return {"seconds": total, "value": 4 * s / total / 1e9, "fpr": float(hn.mean()),
+                "per_op_Mops": {"insert": s / (t1 - t0) / 1e6, "lookup+": s / (t2 - t1) / 1e6,
+                                "lookup-": s / (t3 - t2) / 1e6, "delete": s / (t4 - t3) / 1e6}}
+
+    def describe(self) -> str:
+        return (f"oracle/ C port of the reference kernels on {cpu_model()} x{self.threads} threads; the full "
+                f"2^{self.log2}-slot table prefilled to {100 * (self.n - self.s) / (1 << self.log2):.1f} % "
+                f"load (untimed, {self.setup_s:.1f} s); per step 1/{CPU_SAMPLE} of each op's keys "
+                f"({self.s} keys): insert (to 95 %), lookup+, lookup-, delete, inserts/deletes in the "
+                f"reference's concurrent workers mode, lookups on all threads")
 
 
 def host_threads() -> int:
@@ -149,34 +189,38 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
+def workload_config(log2: int, world: int, eviction: str) -> dict:
+    n = int(0.95 * (1 << log2))
+    return {"workload": "configs[1]: 2^28 slots/GPU f=16 b=16 xor, insert 0->95% then lookup+/-, delete",
+            "slots_per_gpu": 1 << log2, "keys_per_op_per_gpu": n, "fingerprint_bits": 16,
+            "bucket_slots": 16, "policy": "xor", "eviction": eviction,
+            "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
+            "l2": "inputs > L2 (2 GiB key arrays, 512 MiB table vs 126 MB L2); no flush"}
+
+
 def run_reference(args) -> None:
     rank = int(os.environ.get("RANK", 0))
     if rank != 0:
         return
-    import oracle
-
-    oracle.build()
     threads = host_threads()
-    n = int(0.95 * (1 << args.cpu_log2_slots))
+    n = int(0.95 * (1 << args.log2_slots))
     pos, neg = gen_keys(n, 0), gen_keys(n, 0, negative=True)
+    arm = CpuArm(args.log2_slots, pos, neg, threads)
     for _ in range(args.warmup):
-        cpu_protocol(args.cpu_log2_slots, pos, neg, threads)
-    runs = [cpu_protocol(args.cpu_log2_slots, pos, neg, threads) for _ in range(args.steps)]
+        arm.step()
+    runs = [arm.step() for _ in range(args.steps)]
     secs = [r["seconds"] for r in runs]
-    value = 4 * n * len(runs) / sum(secs) / 1e9
-    sample = (f"per step: the step protocol on a 2^{args.cpu_log2_slots}-slot f=16 b=16 xor/bfs table "
-              f"(n={n} keys, same gen_keys streams); insert/delete 1 thread, lookups {threads} threads")
+    value = 4 * arm.s * len(runs) / sum(secs) / 1e9
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
         "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
         "data": "synthetic (reference gen_keys Philox streams)",
-        "config": {"workload": f"cuckoo filter step protocol, 2^{args.cpu_log2_slots} slots sample of configs[1]",
-                   "fingerprint_bits": 16, "bucket_slots": 16, "policy": "xor", "eviction": "bfs",
-                   "load_factor": 0.95, "keys_per_step": 4 * n},
-        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": sample},
+        "config": workload_config(args.log2_slots, args.gpus, args.eviction),
+        "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": arm.describe(),
+                         "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
-        "per_op_Mops": runs[-1]["per_op_Mops"],
+        "per_op_Mops": {k: round(v, 2) for k, v in runs[-1]["per_op_Mops"].items()},
     }
     print(json.dumps(line), flush=True)
 
@@ -363,16 +407,12 @@ def run_ours(args) -> None:
 
     cpu = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        import oracle
-
-        oracle.build()
-        th = host_threads()
-        r = cpu_protocol(args.cpu_log2_slots, pos_h, neg_h, th)
-        cpu = {"value": r["value"], "unit": UNIT, "cores": th, "kind": "port",
-               "sample": (f"oracle/ C restatement of the reference kernels; one step protocol on a "
-                          f"2^{args.cpu_log2_slots}-slot table (n={r['n']}), insert/delete 1 thread, "
-                          f"lookups {th} threads; {r['seconds']:.1f} s"),
+        arm = CpuArm(log2, pos_h, neg_h, host_threads())
+        r = arm.step()
+        cpu = {"value": r["value"], "unit": UNIT, "cores": arm.threads, "kind": "port", "sample": arm.describe(),
+               "cpu": cpu_model(), "step_s": round(r["seconds"], 3),
                "per_op_Mops": {k: round(v, 2) for k, v in r["per_op_Mops"].items()}}
+        del arm
 
     if rank == 0:
         line = {
@@ -380,11 +420,7 @@ def run_ours(args) -> None:
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
             "data": "synthetic (reference gen_keys Philox streams, seed = rank)",
-            "config": {"workload": "configs[1]: 2^28 slots/GPU f=16 b=16 xor, insert 0->95% then lookup+/-, delete",
-                       "slots_per_gpu": 1 << log2, "keys_per_op_per_gpu": n, "fingerprint_bits": f,
-                       "bucket_slots": b, "policy": "xor", "eviction": args.eviction,
-                       "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
-                       "l2": "inputs > L2 (2 GiB key arrays, 512 MiB table vs 126 MB L2); no flush"},
+            "config": workload_config(log2, world, args.eviction),
             "roofline": roofline, "ops": op_stats, "verify": verify,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -403,7 +439,6 @@ def main() -> None:
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--log2-slots", type=int, default=28)
     ap.add_argument("--eviction", choices=["dfs", "bfs"], default="bfs")
-    ap.add_argument("--cpu-log2-slots", type=int, default=24)
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")

@@ -36,7 +36,7 @@
 extern "C" {
 #endif
 
-#define CKF_ABI_VERSION 1
+#define CKF_ABI_VERSION 2
 
 #define CKF_OK 0
 #define CKF_EINVAL (-22)
@@ -52,8 +52,13 @@ extern "C" {
 #define CKF_MODE_SEQUENTIAL 1u   /* one device thread, reference key order:
                                     bit-identical to insert_batch(workers=1) */
 #define CKF_INPUT_HASHED 2u      /* `keys` already holds xxh64(key, seed) */
-#define CKF_FORCE_DIRECT 4u      /* never use the L2-tiled path */
-#define CKF_FORCE_TILED 8u       /* use the L2-tiled path whenever it applies */
+#define CKF_FORCE_DIRECT 4u      /* never use the region (batch) schedule */
+#define CKF_FORCE_TILED 8u       /* use the region schedule whenever its plan applies */
+
+/* Schedules (ckf_schedule) */
+#define CKF_SCHED_DIRECT 0       /* one thread per key, random bucket accesses */
+#define CKF_SCHED_REGION 1       /* bin -> split -> shared-memory probe per table region */
+#define CKF_SCHED_SEQUENTIAL 2   /* parity mode: one device thread, reference order */
 
 /* op ids for ckf_workspace_bytes */
 #define CKF_OP_QUERY 0
@@ -120,11 +125,17 @@ int ckf_hash(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, voi
 int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* fp, uint64_t* i1,
               uint64_t* i2, unsigned flags, void* stream);
 
-/* Scratch bytes for which a batch of n keys runs L2-tiled (binned by bucket
- * region so every random bucket access is served from L2).
+/* Scratch bytes for which a batch of n keys runs the region schedule (keys
+ * binned by table region, every bucket access in shared memory).
  * 0 means this batch runs on the direct kernels and needs no workspace.
  * Passing a smaller (or NULL) workspace to an op also selects the direct path. */
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags);
+
+/* The schedule (CKF_SCHED_*) an op call with these arguments runs, and in how
+ * many back-to-back region runs (*runs; a run holds at most 2^(64-ish)-2 keys,
+ * DESIGN.md §2).  Negative: invalid parameters. */
+int ckf_schedule(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys,
+                 const void* workspace, uint64_t workspace_bytes, uint64_t* runs);
 
 /* Batch insert.  ok[n] is required.  evictions/lost are optional DENSE
  * outputs with the reference's types (int64 / uint64 per key).  records
@@ -169,6 +180,13 @@ int ckf_route_partition(const uint64_t* hashes, uint64_t n, uint32_t shift, uint
 uint64_t ckf_kmer_workspace_bytes(uint64_t len);
 int ckf_kmers(const uint8_t* seq, uint64_t len, uint32_t k, uint64_t* out,
               unsigned long long* n_out, void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* Debug hook for the BFS rollback test (the reference sabotages lane_cas,
+ * pkg/tests/test_filter.py:224-259): the next `count` BFS relocations see a
+ * concurrent writer replace their origin lane with a stale tag right before
+ * the origin CAS, so they roll their copy back and retry.  Pending count out. */
+int ckf_debug_fault_origin_cas(unsigned int count);
+int ckf_debug_faults_pending(unsigned int* count);
 
 /* Host-compiled copies of the shared device semantics (same source as the
  * kernels); used by derive_placement() and by the CPU parity tests. */

@@ -89,6 +89,9 @@ def lib():
         L.ck_delete_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int]
         L.ck_query_batch.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int,
                                      ctypes.c_int]
+        for fn in (L.ck_insert_batch_mt, L.ck_delete_batch_mt):
+            fn.restype = ctypes.c_int64
+            fn.argtypes = [P(CkCfg), u64p, u64p, ctypes.c_int64, u64p, ctypes.c_int, ctypes.c_int]
         L.ck_try_insert.restype = ctypes.c_int64
         L.ck_try_insert.argtypes = [P(CkCfg), u64p, ctypes.c_int64, ctypes.c_uint64]
         L.ck_remove_tag.restype = ctypes.c_int64
@@ -171,6 +174,25 @@ class OracleFilter:
                                      _ptr(ok), _ptr(ev), _ptr(lost), int(hashed))
         self.occupancy += int(n_ok)
         return ok.view(np.bool_), ev, lost
+
+    def insert_batch_mt(self, keys, threads: int, hashed: bool = False) -> np.ndarray:
+        """The reference's workers>1 insert (filter.py:422-438): contiguous chunks,
+        one thread and worker id each, atomic word CASes.  CPU baseline only."""
+        k = _keys(keys)
+        ok = np.zeros(len(k), np.uint8)
+        n_ok = lib().ck_insert_batch_mt(ctypes.byref(self.cfg), _ptr(self.words), _ptr(k), len(k),
+                                        _ptr(ok), int(hashed), int(threads))
+        self.occupancy += int(n_ok)
+        return ok.view(np.bool_)
+
+    def delete_batch_mt(self, keys, threads: int, hashed: bool = False) -> np.ndarray:
+        """The reference's workers>1 delete (filter.py:483-500)."""
+        k = _keys(keys)
+        out = np.zeros(len(k), np.uint8)
+        n_ok = lib().ck_delete_batch_mt(ctypes.byref(self.cfg), _ptr(self.words), _ptr(k), len(k),
+                                        _ptr(out), int(hashed), int(threads))
+        self.occupancy -= int(n_ok)
+        return out.view(np.bool_)
 
     def query_batch(self, keys, threads: int = 1, hashed: bool = False) -> np.ndarray:
         k = _keys(keys)

@@ -16,10 +16,14 @@
  * Integer discipline follows the reference (K:17-20): every value is uint64_t
  * with wrapping arithmetic; slot/word indexes are int64_t.
  *
- * Concurrency: none.  The reference's batch insert/delete run sequentially
- * with the GIL held (K:510-549, filter.py:416-421), so the oracle is a single
- * sequential loop for mutations; the read-only query batch is split across
- * POSIX threads exactly like filter.py:458-469 does with Python threads.
+ * Concurrency: the parity functions are sequential, like the reference's
+ * workers=1 batch insert/delete (K:510-549, filter.py:416-421); the read-only
+ * query batch is split across POSIX threads exactly like filter.py:458-469
+ * does with Python threads.  ck_insert_batch_mt / ck_delete_batch_mt restate
+ * the reference's workers>1 mode (filter.py:422-438, 483-500: contiguous
+ * chunks, one worker id per chunk for the eviction PRNG) with the word CASes
+ * of K:158-272 as C11 atomics -- the CPU baseline of bench.py, never a parity
+ * reference (concurrent outcomes are schedule-dependent).
  */
 #include <pthread.h>
 #include <stdint.h>
@@ -402,6 +406,222 @@ void ck_query_batch(const ck_cfg* c, const u64* words, const u64* keys, i64 n, u
   for (int t = 0; t < threads; ++t) pthread_join(tid[t], NULL);
   free(tid);
   free(jobs);
+}
+
+/* ---------------- concurrent workers (filter.py:422-438, 483-500) ----------------
+ * The same operations with every word access atomic: a lane is claimed,
+ * cleared or replaced by a compare-and-swap of its whole word (K:158-254). */
+
+static inline u64 aload(const u64* p) { return __atomic_load_n(p, __ATOMIC_RELAXED); }
+static inline int acas(u64* p, u64* expect, u64 desired) {
+  return __atomic_compare_exchange_n(p, expect, desired, 0, __ATOMIC_RELAXED, __ATOMIC_RELAXED);
+}
+
+static i64 bucket_put_at(u64* words, i64 base, u64 tag, const ck_cfg* c) {
+  i64 start = (i64)(tag % c->b) / c->tpw;
+  for (i64 k = 0; k < c->wpb; ++k) {
+    i64 wk = (start + k) % c->wpb;
+    u64 w = aload(words + base + wk);
+    for (;;) {
+      u64 z = lane_zeros(w, c->high);
+      if (!z) break;
+      i64 s = lowest_lane(z, c->f);
+      if (acas(words + base + wk, &w, lane_set(w, s, tag, c->f))) return wk * c->tpw + s;
+    }
+  }
+  return -1;
+}
+
+static i64 bucket_take_at(u64* words, i64 base, u64 tag, const ck_cfg* c) {
+  u64 pat = lane_bcast(tag, c->f);
+  i64 start = (i64)(tag % c->b) / c->tpw;
+  for (i64 k = 0; k < c->wpb; ++k) {
+    i64 wk = (start + k) % c->wpb;
+    u64 w = aload(words + base + wk);
+    for (;;) {
+      u64 mm = lane_zeros(w ^ pat, c->high);
+      if (!mm) break;
+      i64 s = lowest_lane(mm, c->f);
+      if (acas(words + base + wk, &w, lane_set(w, s, 0, c->f))) return wk * c->tpw + s;
+    }
+  }
+  return -1;
+}
+
+/* lane_cas (K:247-254): replace lane s of word p only while it holds `expect` */
+static int lane_cas_at(u64* p, i64 s, u64 expect, u64 repl, u64 f) {
+  u64 w = aload(p);
+  for (;;) {
+    if (lane_get(w, s, f) != expect) return 0;
+    if (acas(p, &w, lane_set(w, s, repl, f))) return 1;
+  }
+}
+
+static int insert_hash_at(u64* words, u64 h, const ck_cfg* c, i64* rounds, u64* lost, i64* cand_slot,
+                          u64* cand_tag) {
+  u64 fp, i1, i2;
+  place_hash(h, c, &fp, &i1, &i2);
+  u64 tag1 = fp;
+  u64 tag2 = make_tag(fp, c->policy == 1 ? 1u : 0u, c);
+  *rounds = 0;
+  *lost = 0;
+  if (bucket_put_at(words, (i64)i1 * c->wpb, tag1, c) >= 0) return 1;
+  if (bucket_put_at(words, (i64)i2 * c->wpb, tag2, c) >= 0) return 1;
+  u64 st = ck_rng_init(c->seed, h, c->worker) + GOLDEN;
+  u64 cur_b = i1, cur_tag = tag1;
+  if (ck_smix(st) & 1u) {
+    cur_b = i2;
+    cur_tag = tag2;
+  }
+  if (c->strategy == 0) { /* DFS: atomic lane exchange (swap_slot, K:232-244) */
+    for (i64 n = 1; n <= c->max_evictions; ++n) {
+      st += GOLDEN;
+      i64 victim = (i64)(ck_smix(st) % c->b);
+      u64* p = words + (i64)cur_b * c->wpb + victim / c->tpw;
+      u64 w = aload(p), old;
+      do {
+        old = lane_get(w, victim % c->tpw, c->f);
+      } while (!acas(p, &w, lane_set(w, victim % c->tpw, cur_tag, c->f)));
+      if (old == 0) {
+        *rounds = n;
+        return 1;
+      }
+      u64 nc;
+      cur_b = alt_bucket(cur_b, tag_payload(old, c), tag_choice(old, c), c, &nc);
+      cur_tag = make_tag(tag_payload(old, c), nc, c);
+      if (bucket_put_at(words, (i64)cur_b * c->wpb, cur_tag, c) >= 0) {
+        *rounds = n;
+        return 1;
+      }
+    }
+    *rounds = c->max_evictions;
+    *lost = tag_payload(cur_tag, c);
+    return 0;
+  }
+  i64 limit = (i64)c->b / 2;
+  if (limit < 1) limit = 1;
+  for (i64 n = 1; n <= c->max_evictions; ++n) { /* BFS (K:391-436) */
+    st += GOLDEN;
+    i64 start = (i64)(ck_smix(st) % c->b);
+    i64 base = (i64)cur_b * c->wpb;
+    i64 cnt = 0;
+    for (i64 j = 0; j < (i64)c->b && cnt < limit; ++j) {
+      i64 s = (start + j) % (i64)c->b;
+      u64 t = lane_get(aload(words + base + s / c->tpw), s % c->tpw, c->f);
+      if (t) {
+        cand_slot[cnt] = s;
+        cand_tag[cnt] = t;
+        ++cnt;
+      }
+    }
+    if (cnt == 0) {
+      if (bucket_put_at(words, base, cur_tag, c) >= 0) {
+        *rounds = n;
+        return 1;
+      }
+      continue;
+    }
+    i64 chosen = -1;
+    u64 alt_b = 0, alt_tag = 0;
+    for (i64 j = 0; j < cnt; ++j) {
+      u64 tc;
+      u64 tb = alt_bucket(cur_b, tag_payload(cand_tag[j], c), tag_choice(cand_tag[j], c), c, &tc);
+      int room = 0;
+      for (i64 k = 0; k < c->wpb && !room; ++k) room = lane_zeros(aload(words + (i64)tb * c->wpb + k), c->high) != 0;
+      if (room) {
+        chosen = j;
+        alt_b = tb;
+        alt_tag = make_tag(tag_payload(cand_tag[j], c), tc, c);
+        break;
+      }
+    }
+    if (chosen >= 0) {
+      i64 aslot = bucket_put_at(words, (i64)alt_b * c->wpb, alt_tag, c);
+      if (aslot < 0) continue;
+      i64 os = cand_slot[chosen];
+      if (lane_cas_at(words + base + os / c->tpw, os % c->tpw, cand_tag[chosen], cur_tag, c->f)) {
+        *rounds = n;
+        return 1;
+      }
+      lane_cas_at(words + (i64)alt_b * c->wpb + aslot / c->tpw, aslot % c->tpw, alt_tag, 0, c->f);
+      continue;
+    }
+    i64 os = cand_slot[cnt - 1];
+    u64 ct = cand_tag[cnt - 1];
+    if (!lane_cas_at(words + base + os / c->tpw, os % c->tpw, ct, cur_tag, c->f)) continue;
+    u64 nc;
+    cur_b = alt_bucket(cur_b, tag_payload(ct, c), tag_choice(ct, c), c, &nc);
+    cur_tag = make_tag(tag_payload(ct, c), nc, c);
+  }
+  *rounds = c->max_evictions;
+  *lost = tag_payload(cur_tag, c);
+  return 0;
+}
+
+typedef struct {
+  ck_cfg c; /* private copy: worker id = chunk index (filter.py:428) */
+  u64* words;
+  const u64* keys;
+  uint8_t* out;
+  i64 lo, hi;
+  int hashed, del;
+  i64 n_ok;
+} mjob;
+
+static void* mutate_worker(void* arg) {
+  mjob* j = (mjob*)arg;
+  i64 lim = (i64)j->c.b / 2 > 0 ? (i64)j->c.b / 2 : 1;
+  i64* cs = (i64*)malloc(sizeof(i64) * lim);
+  u64* ct = (u64*)malloc(sizeof(u64) * lim);
+  for (i64 i = j->lo; i < j->hi; ++i) {
+    u64 h = key_hash(j->keys[i], &j->c, j->hashed);
+    int good;
+    if (j->del) {
+      u64 fp, i1, i2;
+      place_hash(h, &j->c, &fp, &i1, &i2);
+      u64 tag2 = j->c.policy == 1 ? make_tag(fp, 1u, &j->c) : fp;
+      good = bucket_take_at(j->words, (i64)i1 * j->c.wpb, fp, &j->c) >= 0 ||
+             bucket_take_at(j->words, (i64)i2 * j->c.wpb, tag2, &j->c) >= 0;
+    } else {
+      i64 r;
+      u64 l;
+      good = insert_hash_at(j->words, h, &j->c, &r, &l, cs, ct);
+    }
+    if (j->out) j->out[i] = (uint8_t)good;
+    j->n_ok += good;
+  }
+  free(cs);
+  free(ct);
+  return NULL;
+}
+
+static i64 mutate_mt(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* out, int hashed, int del,
+                     int threads) {
+  if (threads < 1) threads = 1;
+  pthread_t* tid = (pthread_t*)malloc(sizeof(pthread_t) * threads);
+  mjob* jobs = (mjob*)malloc(sizeof(mjob) * threads);
+  for (int t = 0; t < threads; ++t) {
+    jobs[t] = (mjob){*c, words, keys, out, (t * n) / threads, ((t + 1) * n) / threads, hashed, del, 0};
+    jobs[t].c.worker = (u64)t;
+    pthread_create(&tid[t], NULL, mutate_worker, &jobs[t]);
+  }
+  i64 n_ok = 0;
+  for (int t = 0; t < threads; ++t) {
+    pthread_join(tid[t], NULL);
+    n_ok += jobs[t].n_ok;
+  }
+  free(tid);
+  free(jobs);
+  return n_ok;
+}
+
+i64 ck_insert_batch_mt(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* ok, int hashed, int threads) {
+  return mutate_mt(c, words, keys, n, ok, hashed, 0, threads);
+}
+
+i64 ck_delete_batch_mt(const ck_cfg* c, u64* words, const u64* keys, i64 n, uint8_t* out, int hashed,
+                       int threads) {
+  return mutate_mt(c, words, keys, n, out, hashed, 1, threads);
 }
 
 /* Scalar helpers the tests pin individually (K:158-272). */

@@ -16,7 +16,7 @@ from pathlib import Path
 _HERE = Path(__file__).resolve().parent
 LIB_PATH = _HERE / "libckf.so"
 
-ABI_VERSION = 1
+ABI_VERSION = 2
 OK = 0
 EINVAL = -22
 
@@ -30,6 +30,11 @@ MODE_SEQUENTIAL = 1
 INPUT_HASHED = 2
 FORCE_DIRECT = 4
 FORCE_TILED = 8
+
+SCHED_DIRECT = 0
+SCHED_REGION = 1
+SCHED_SEQUENTIAL = 2
+SCHED_NAMES = {SCHED_DIRECT: "direct", SCHED_REGION: "region", SCHED_SEQUENTIAL: "sequential"}
 
 OP_QUERY = 0
 OP_INSERT = 1
@@ -74,6 +79,8 @@ SIGNATURES = {
     "ckf_hash": (ctypes.c_int, [_vp, _u64, _u64, _vp, _vp]),
     "ckf_place": (ctypes.c_int, [_P, _vp, _u64, _vp, _vp, _vp, ctypes.c_uint, _vp]),
     "ckf_workspace_bytes": (_u64, [_P, _u64, ctypes.c_int, ctypes.c_uint]),
+    "ckf_schedule": (ctypes.c_int, [_P, _u64, ctypes.c_int, ctypes.c_uint, _vp, _vp, _u64,
+                                    ctypes.POINTER(_u64)]),
     "ckf_insert": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, _vp, _vp,
                                   _vp, _u64, ctypes.c_uint, _vp]),
     "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.c_uint, _vp]),
@@ -83,6 +90,8 @@ SIGNATURES = {
     "ckf_route_partition": (ctypes.c_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp, _u64, _vp]),
     "ckf_kmer_workspace_bytes": (_u64, [_u64]),
     "ckf_kmers": (ctypes.c_int, [_vp, _u64, _u32, _vp, _vp, _vp, _u64, _vp]),
+    "ckf_debug_fault_origin_cas": (ctypes.c_int, [ctypes.c_uint]),
+    "ckf_debug_faults_pending": (ctypes.c_int, [ctypes.POINTER(ctypes.c_uint)]),
     "ckf_host_hash": (_u64, [_u64, _u64]),
     "ckf_host_place": (None, [_P, _u64, ctypes.POINTER(_u64), ctypes.POINTER(_u64),
                               ctypes.POINTER(_u64)]),

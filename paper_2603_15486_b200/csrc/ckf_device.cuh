@@ -290,6 +290,27 @@ __device__ bool lane_cas(uint64_t* p, int lane, uint64_t expect, uint64_t repl) 
   }
 }
 
+// Debug hook (ckf_debug_fault_origin_cas, the rollback test): while armed, a
+// BFS relocation's origin lane is first overwritten by a "concurrent writer"
+// with a stale tag, so the chain's origin CAS loses and rolls its copy back --
+// the GPU counterpart of the reference's sabotaged lane_cas
+// (pkg/tests/test_filter.py:224-259).  One relaxed load when disarmed.
+__device__ unsigned int g_fault_origin_cas = 0;
+
+template <int F>
+__device__ __forceinline__ void fault_origin_writer(uint64_t* p, int lane, uint64_t expect) {
+  unsigned int v = *(volatile unsigned int*)&g_fault_origin_cas;
+  while (v) {
+    const unsigned int old = atomicCAS(&g_fault_origin_cas, v, v - 1);
+    if (old == v) {
+      const uint64_t stale = (expect ^ 1u) ? (expect ^ 1u) : 2u;
+      lane_cas<F>(p, lane, expect, stale);
+      return;
+    }
+    v = old;
+  }
+}
+
 template <int F>
 __device__ bool bucket_has_empty(const uint64_t* words, uint64_t bucket, const Geo& g) {
   const uint64_t* p = words + bucket * g.wpb;
@@ -389,6 +410,7 @@ __device__ Outcome evict_chain(uint64_t* words, uint64_t h, uint64_t fp, uint64_
       int aslot = try_insert_rt<F>(words, alt_b, alt_tag, g);
       if (aslot < 0) continue;  // the free lane raced away
       uint32_t os = cslot[chosen];
+      fault_origin_writer<F>(base + os / L::kTpw, os % L::kTpw, ctag[chosen]);
       if (lane_cas<F>(base + os / L::kTpw, os % L::kTpw, ctag[chosen], cur_tag)) return {1u, n, 0};
       // origin lane changed underfoot: remove the copy we just made
       lane_cas<F>(words + alt_b * g.wpb + aslot / L::kTpw, aslot % L::kTpw, alt_tag, 0);
@@ -446,8 +468,38 @@ __device__ __forceinline__ uint32_t nth_candidate(uint64_t rot, uint32_t j, uint
   return s >= B ? s - B : s;
 }
 
+// Room map of the batch schedule (ckf_region.cuh): bit i of `bits` says
+// whether bucket i had an empty lane when the probe passes last wrote it (the
+// insert's phase-1 probe writes every region, phase 2 rewrites the regions it
+// mutates).  The BFS asks it "does the candidate's alternate bucket have room"
+// (bucket_has_empty, K:225-230) from L2 instead of fetching the bucket from
+// HBM; the chains keep it current with fire-and-forget atomics.  A stale
+// answer is one a concurrent insert could have produced (the chain's insert
+// then finds the bucket full and the round retries, K:416-418).
+// bits == nullptr: no map.
+struct RoomMap {
+  uint32_t* bits;
+};
+
+// a successful insert into bucket b whose snapshot had `empties` empty lanes
+__device__ __forceinline__ void rm_filled(const RoomMap& rm, uint64_t b, uint32_t empties) {
+  if (rm.bits && empties <= 1) atomicAnd(rm.bits + (b >> 5), ~(1u << (b & 31)));
+}
+__device__ __forceinline__ void rm_freed(const RoomMap& rm, uint64_t b) {
+  if (rm.bits) atomicOr(rm.bits + (b >> 5), 1u << (b & 31));
+}
+
+template <int F, int WPB>
+__device__ __forceinline__ uint32_t empty_lanes(const uint64_t (&w)[WPB]) {
+  uint32_t c = 0;
+#pragma unroll
+  for (int j = 0; j < WPB; ++j) c += __popcll(Lanes<F>::zeros(w[j]));
+  return c;
+}
+
 template <int F, int WPB, int POL>
-__device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2, const Geo& g) {
+__device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2, const Geo& g,
+                                 const RoomMap rm = RoomMap{nullptr}) {
   using L = Lanes<F>;
   constexpr int kTpw = L::kTpw;
   constexpr uint32_t kB = WPB * kTpw;
@@ -493,36 +545,74 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
     const uint32_t pc = (uint32_t)__popcll(rot);
     const uint32_t cnt = pc < kLim ? pc : kLim;
     if (cnt == 0) {  // drained by concurrent deletes: take a direct slot
-      if (try_insert_snap<F, WPB>(words, cur_b, cur_tag, cw) >= 0) return {1u, n, 0};
+      const uint32_t e = empty_lanes<F, WPB>(cw);
+      if (try_insert_snap<F, WPB>(words, cur_b, cur_tag, cw) >= 0) {
+        rm_filled(rm, cur_b, e);
+        return {1u, n, 0};
+      }
       continue;
     }
     int chosen = -1;
     uint64_t alt_b = 0, alt_tag = 0, aw_chosen[WPB];
-    for (uint32_t c0 = 0; c0 < cnt && chosen < 0; c0 += kEvictFetch) {
-      uint64_t aw[kEvictFetch][WPB], ab[kEvictFetch], at[kEvictFetch];
+    if (rm.bits) {
+      // every candidate's room bit at once (independent L2 loads of the
+      // map), then the first candidate with room in the reference order
+      // (K:407-414); only that candidate's bucket is fetched
+      uint32_t word[kLim], bit[kLim];
+      uint64_t rr = rot;
 #pragma unroll
-      for (int q = 0; q < kEvictFetch; ++q) {
-        if (c0 + q >= cnt) continue;
-        const uint32_t s = nth_candidate<kB>(rot, c0 + q, start);
+      for (uint32_t c = 0; c < kLim; ++c) {
+        word[c] = bit[c] = 0;
+        if (c >= cnt) continue;
+        uint32_t s = (uint32_t)(__ffsll((long long)rr) - 1) + start;
+        s = s >= kB ? s - kB : s;
+        rr &= rr - 1;
+        const uint64_t ct = L::get(snap_word<WPB>(cw, s / kTpw), s % kTpw);
+        uint64_t tc;
+        const uint64_t ab = alt_index<POL>(cur_b, tag_fp(ct, g), tag_choice(ct, g), g, tc);
+        word[c] = __ldcg(rm.bits + (ab >> 5));
+        bit[c] = (uint32_t)(ab & 31);
+      }
+      uint32_t roomm = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kLim; ++c) roomm |= ((word[c] >> bit[c]) & 1u) << c;
+      if (roomm) {
+        chosen = __ffs((int)roomm) - 1;
+        const uint32_t s = nth_candidate<kB>(rot, (uint32_t)chosen, start);
         const uint64_t ct = L::get(snap_word<WPB>(cw, s / kTpw), s % kTpw);
         uint64_t tc;
         const uint64_t cfp = tag_fp(ct, g);
-        ab[q] = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, tc);
-        at[q] = make_tag(cfp, tc, g);
-        ld_bucket_rw<WPB>(words + ab[q] * WPB, aw[q]);
+        alt_b = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, tc);
+        alt_tag = make_tag(cfp, tc, g);
+        ld_bucket_rw<WPB>(words + alt_b * WPB, aw_chosen);
       }
+    } else {
+      for (uint32_t c0 = 0; c0 < cnt && chosen < 0; c0 += kEvictFetch) {
+        uint64_t aw[kEvictFetch][WPB], ab[kEvictFetch], at[kEvictFetch];
 #pragma unroll
-      for (int q = 0; q < kEvictFetch; ++q) {
-        if (chosen >= 0 || c0 + q >= cnt) continue;
-        uint64_t any = 0;
+        for (int q = 0; q < kEvictFetch; ++q) {
+          if (c0 + q >= cnt) continue;
+          const uint32_t s = nth_candidate<kB>(rot, c0 + q, start);
+          const uint64_t ct = L::get(snap_word<WPB>(cw, s / kTpw), s % kTpw);
+          uint64_t tc;
+          const uint64_t cfp = tag_fp(ct, g);
+          ab[q] = alt_index<POL>(cur_b, cfp, tag_choice(ct, g), g, tc);
+          at[q] = make_tag(cfp, tc, g);
+          ld_bucket_rw<WPB>(words + ab[q] * WPB, aw[q]);
+        }
 #pragma unroll
-        for (int j = 0; j < WPB; ++j) any |= L::zeros(aw[q][j]);
-        if (any) {
-          chosen = (int)(c0 + q);
-          alt_b = ab[q];
-          alt_tag = at[q];
+        for (int q = 0; q < kEvictFetch; ++q) {
+          if (chosen >= 0 || c0 + q >= cnt) continue;
+          uint64_t any = 0;
 #pragma unroll
-          for (int j = 0; j < WPB; ++j) aw_chosen[j] = aw[q][j];
+          for (int j = 0; j < WPB; ++j) any |= L::zeros(aw[q][j]);
+          if (any) {
+            chosen = (int)(c0 + q);
+            alt_b = ab[q];
+            alt_tag = at[q];
+#pragma unroll
+            for (int j = 0; j < WPB; ++j) aw_chosen[j] = aw[q][j];
+          }
         }
       }
     }
@@ -531,10 +621,17 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
     const uint64_t otag = L::get(ow, os % kTpw);
     if (chosen >= 0) {
       // two-step relocation: copy the candidate out, then swap ourselves in
+      const uint32_t e = empty_lanes<F, WPB>(aw_chosen);
       const int aslot = try_insert_snap<F, WPB>(words, alt_b, alt_tag, aw_chosen);
-      if (aslot < 0) continue;  // the free lane raced away
+      if (aslot < 0) {  // the free lane raced away
+        if (rm.bits) rm_filled(rm, alt_b, 0);
+        continue;
+      }
+      rm_filled(rm, alt_b, e);
+      fault_origin_writer<F>(base + os / kTpw, os % kTpw, otag);
       if (lane_cas_from<F>(base + os / kTpw, os % kTpw, otag, cur_tag, ow)) return {1u, n, 0};
       lane_cas<F>(words + alt_b * WPB + aslot / kTpw, aslot % kTpw, alt_tag, 0);  // rollback
+      rm_freed(rm, alt_b);
       continue;
     }
     // nobody has room: evict the last candidate and deepen (K:427-434)
@@ -549,8 +646,8 @@ __device__ Outcome evict_chain_t(uint64_t* words, uint64_t h, uint64_t fp, uint6
 
 template <int F, int WPB, int POL>
 __device__ __forceinline__ Outcome evict_any(uint64_t* words, uint64_t h, uint64_t fp, uint64_t i1, uint64_t i2,
-                                             const Geo& g) {
-  if constexpr (WPB > 0) return evict_chain_t<F, WPB, POL>(words, h, fp, i1, i2, g);
+                                             const Geo& g, const RoomMap rm = RoomMap{nullptr}) {
+  if constexpr (WPB > 0) return evict_chain_t<F, WPB, POL>(words, h, fp, i1, i2, g, rm);
   else return evict_chain<F, POL>(words, h, fp, i1, i2, g);
 }
 

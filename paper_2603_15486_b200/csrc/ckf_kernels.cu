@@ -7,11 +7,10 @@
 // (reference filter.py:130, wordops.py:1-16).  With f=16, b=16 a bucket is one
 // 32-byte sector.
 //
-// Schedules, chosen per call (choose() below):
+// Schedules, chosen per call (choose() below; ckf_schedule() reports it):
 //   region (ckf_region.cuh)  large batches on large tables: bin -> split ->
 //                            shared-memory probe per table region, twice
 //                            (primary, then alternate buckets), + eviction;
-//   L2-tiled (ckf_tiled.cuh) round-1 schedule, CKF_SCHED=l2 (comparison);
 //   direct (this file)       one thread per key:
 //     query_kernel   <F,WPB,POL,KPT>  read-only 256-bit bucket loads
 //     insert_kernel  <F,WPB,POL>      TryInsert i1 then i2 with a 64-bit
@@ -35,7 +34,7 @@
 #include "../../include/ckf.h"
 #include "ckf_semantics.cuh"
 #include "ckf_device.cuh"
-#include "ckf_tiled.cuh"
+#include "ckf_ops.cuh"
 #include "ckf_region.cuh"
 
 namespace ckf {
@@ -198,23 +197,29 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
 }
 
 // Eviction pass over the queued keys (the ~4% whose pair was full at 95% load).
+constexpr int kEvictBlocks = 3;  // resident blocks per SM (<= 85 registers: the BFS chain's snapshots)
+// Queue entries [*qstart, n_queued) belong to this run (a chunk of the call
+// whose keys start at batch index ibase; keys / ok / ev / lost are the run's).
 template <int F, int WPB, int POL>
-__global__ void __launch_bounds__(kBlock) evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
+__global__ void __launch_bounds__(kBlock, kEvictBlocks) evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
                                                        int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
                                                        ckf_record* __restrict__ rec, uint64_t cap,
                                                        ckf_counters* ctr, long long* occ,
-                                                       const uint64_t* __restrict__ keys, bool hashed) {
+                                                       const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
+                                                       const unsigned long long* qstart, RoomMap rm) {
   const unsigned long long queued = *(volatile unsigned long long*)&ctr->n_queued;
   const uint64_t cnt = queued < cap ? queued : cap;
+  const uint64_t r0 = qstart ? *qstart : 0;
   uint32_t n_ok = 0;
-  for (uint64_t r = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < cnt; r += (uint64_t)gridDim.x * blockDim.x) {
-    const uint64_t i = rec[r].index;
+  for (uint64_t r = r0 + blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; r < cnt;
+       r += (uint64_t)gridDim.x * blockDim.x) {
+    const uint64_t i = rec[r].index - ibase;
     uint64_t h = rec[r].lost;  // the key hash parked by the queueing pass, or kRehash
     if (h == kRehash) h = load_hash(keys, i, g.seed, hashed);
     uint64_t fp, i1, i2;
     place<POL>(h, g, fp, i1, i2);
-    Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
-    rec[r] = ckf_record{i, o.lost, o.rounds, o.ok};
+    Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g, rm);
+    rec[r] = ckf_record{i + ibase, o.lost, o.rounds, o.ok};
     n_ok += o.ok;
     if (!o.ok) ok[i] = 0;  // queued keys enter with ok = 1 (scattered byte writes only on failure)
     if (ev) ev[i] = o.rounds;
@@ -363,136 +368,24 @@ static int dispatch3(const ckf_params* p, const void* words, A... a) {
 
 
 // ---------------------------------------------------------------------------
-// L2-tiled execution: plan + workspace layout (host side; see ckf_tiled.cuh)
+// shared-memory region schedule: plan + workspace layout (see ckf_region.cuh)
 // ---------------------------------------------------------------------------
 
-constexpr uint64_t kRegionBytes = 2ull << 20;   // table bytes per bin
-constexpr uint64_t kTiledMinTable = 48ull << 20; // below this the table is L2-resident anyway
-
-struct Layout {
-  uint64_t cnt1, cnt2, bin1, bin2, bits, total;
-};
+constexpr uint64_t kRegionMinTable = 48ull << 20;  // below this the table is L2-resident anyway
+constexpr uint32_t kMaxF2 = 512;                   // fine regions per coarse region (split bins)
 
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
 
-// Developer knobs for sweeps (tools/sweep_tiled.py): CKF_REGION_KB, CKF_BIN_GROUP,
-// CKF_TILED_AUTO (0 disables the automatic choice of the tiled path).
+// Developer knobs: CKF_REGION_KB (fine-region bytes), CKF_TILED_AUTO (0
+// disables the automatic choice of the region schedule), CKF_MAX_RUN_KEYS (a
+// smaller run size, so tests cover calls split into several region runs).
 static uint64_t env_u64(const char* name, uint64_t dflt) {
   const char* v = getenv(name);
   return v && *v ? strtoull(v, nullptr, 10) : dflt;
 }
 
-// Binning plan; ok=false when the batch cannot be tiled.
-static Plan make_plan(const ckf_params* p, uint64_t n, unsigned flags, bool& ok) {
-  Plan pl{};
-  ok = false;
-  const uint64_t m = p->bucket_count;
-  const uint64_t bucket_bytes = p->words_per_bucket * 8ull;
-  const uint64_t table = m * bucket_bytes;
-  const bool forced = (flags & CKF_FORCE_TILED) != 0;
-  const uint64_t region_pref = env_u64("CKF_REGION_KB", kRegionBytes >> 10) << 10;
-  // small forced tables still get ~64 bins so the multi-bin logic is exercised
-  const uint64_t region = forced && table < 64 * region_pref ? (table / 64 ? table / 64 : 1) : region_pref;
-  uint64_t rb = region / bucket_bytes;
-  if (rb < 2) rb = 2;
-  const uint64_t max_rb = 1ull << (32 - p->payload_bits);  // bucket offset bits in a record
-  if (rb > max_rb) rb = max_rb;
-  uint64_t R = (m + rb - 1) / rb;
-  if (R > (uint64_t)kMaxBins) {
-    R = kMaxBins;
-    rb = (m + R - 1) / R;
-    if (rb > max_rb) return pl;
-  }
-  rb = (m + R - 1) / R;  // balance the regions
-  R = (m + rb - 1) / rb;
-  if (rb < 2) return pl;
-  pl.rb = (uint32_t)rb;
-  pl.R = (uint32_t)R;
-  pl.pb = p->payload_bits;
-  pl.div_magic = ~0ull / rb + 1;  // Lemire fastdiv: exact bucket / rb for bucket < 2^32
-  pl.group = (uint32_t)env_u64("CKF_BIN_GROUP", 8);
-  if (pl.group < 1) pl.group = 1;
-  const double per = (double)n / (double)R;
-  pl.cap = ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + 1) & ~1ull;  // even: 16 B-aligned bins
-  pl.tiles_per_bin = (uint32_t)((pl.cap + kTile - 1) / kTile);
-  ok = true;
-  return pl;
-}
-
-static bool tiled_applies(const ckf_params* p, uint64_t n, unsigned flags) {
-  if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
-  const uint32_t wpb = p->words_per_bucket;
-  if (wpb != 2 && wpb != 4 && wpb != 8) return false;
-  if (p->bucket_count > 0xFFFFFFFFull || p->bucket_count < 64 || n >= 0xFFFFFFFFull || n == 0) return false;
-  if (p->payload_bits > 24) return false;  // record = idx:32 | offset | fp
-  if (!(flags & CKF_FORCE_TILED)) {
-    if (!env_u64("CKF_TILED_AUTO", 1)) return false;
-    const uint64_t table = p->bucket_count * wpb * 8ull;
-    // enough keys per bucket that binning turns re-fetches into L2 hits
-    if (table < kTiledMinTable || n < p->bucket_count) return false;
-  }
-  bool ok;
-  make_plan(p, n, flags, ok);
-  return ok;
-}
-
-static Layout layout_for(const Plan& pl, uint64_t n, int op) {
-  Layout L{};
-  L.cnt1 = 0;
-  L.cnt2 = align256((uint64_t)pl.R * kCntStride * 4);
-  uint64_t off = 2 * L.cnt2;
-  const uint64_t recs = (uint64_t)pl.R * pl.cap;
-  L.bin1 = off;
-  off = align256(off + recs * 8);
-  L.bin2 = off;
-  off = align256(off + recs * 8);
-  L.bits = off;
-  if (op != CKF_OP_INSERT) off = align256(off + (n + 31) / 32 * 4);
-  L.total = off;
-  return L;
-}
-
-static Work work_view(void* ws, const Layout& L) {
-  char* b = (char*)ws;
-  return Work{(uint32_t*)(b + L.cnt1), (uint32_t*)(b + L.cnt2), (uint64_t*)(b + L.bin1), (uint64_t*)(b + L.bin2),
-              (uint32_t*)(b + L.bits)};
-}
-
-// Tiled run of one op: pass A/B/C (+ bit expansion for query/delete).
-template <int OP, int F, int WPB, int POL>
-static int run_tiled(const Geo& g, const Plan& pl, const Layout& L, void* ws, uint64_t* words, const uint64_t* keys,
-                     uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out, cudaStream_t s) {
-  Work w = work_view(ws, L);
-  if (cudaMemsetAsync(ws, 0, L.bin1, s) != cudaSuccess) return cuda_error();  // bin counters
-  if (OP != OP_INSERT) {
-    if (cudaMemsetAsync(w.bits, 0, (n + 31) / 32 * 4, s) != cudaSuccess) return cuda_error();
-    sk.bits = w.bits;
-  }
-  sk.keys = keys;
-  sk.hashed = hashed;
-  tile_bin_kernel<OP, F, WPB, POL><<<grid_for(n, kTile, kTileMinBlocks), kTileThreads, 0, s>>>(g, pl, words, keys, n,
-                                                                                             hashed, w, sk, occ);
-  int st = status();
-  if (st) return st;
-  const uint64_t tiles = (uint64_t)pl.R * pl.tiles_per_bin;
-  const unsigned gt = grid_for(tiles, 1, kTileMinBlocks);
-  tile_probe1_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
-  if ((st = status())) return st;
-  tile_probe2_kernel<OP, F, WPB, POL><<<gt, kTileThreads, 0, s>>>(g, pl, words, w, sk, occ);
-  if ((st = status())) return st;
-  if (OP != OP_INSERT) {
-    expand_bits_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out);
-    st = status();
-  }
-  return st;
-}
-
-// ---------------------------------------------------------------------------
-// shared-memory region schedule: plan + workspace layout (see ckf_region.cuh)
-// ---------------------------------------------------------------------------
-
 struct RLayout {
-  uint64_t cnt1, cntf, bin_ctr_end, n_miss, mode, ctr_end, bin1, binf, miss, bits, total;
+  uint64_t cnt1, cntf, bin_ctr_end, n_miss, mode, ctr_end, qstart, room, bin1, binf, miss, bits, total;
 };
 
 static uint32_t ceil_log2(uint64_t x) {
@@ -505,7 +398,10 @@ constexpr uint32_t kMaxProbeGrid = 1024;
 
 static uint64_t even_cap(double per) { return ((uint64_t)(per + 4.0 * std::sqrt(per) + 64.0) + 1) & ~1ull; }
 
-// Region plan; ok=false when the schedule does not apply to this table.
+// Region plan for a call of n keys; ok=false when the schedule does not apply
+// to this table.  The plan covers one run of pl.chunk keys; larger calls run
+// ceil(n / chunk) of them back to back (the record's index field holds
+// 64 - ish bits).
 static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags, bool& ok) {
   RPlan pl{};
   ok = false;
@@ -513,7 +409,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   if (wpb != 2 && wpb != 4 && wpb != 8) return pl;
   const uint64_t m = p->bucket_count;
   const uint32_t pb = p->payload_bits;
-  if (pb > 24 || m < 2 || m > (1ull << 32) || n == 0 || n >= 0xFFFFFFFFull) return pl;
+  if (pb > 24 || m < 2 || m > (1ull << 32) || n == 0) return pl;
   const uint64_t bbytes = wpb * 8ull;
   uint32_t lrb = 0;
   const uint64_t smem = env_u64("CKF_REGION_KB", kRegionSmem >> 10) << 10;
@@ -524,30 +420,40 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
     if (lrb > cap) lrb = cap;
   }
   if (lrb < 1) lrb = 1;
-  if (lrb + pb > 31) lrb = 31 - pb;
-  // coarse regions: ~512 of them, at most 2^(31-pb) buckets each (record offset bits)
+  // coarse regions: at most kRMaxCoarse of them, each split into F2 <= kMaxF2 fine ones
   uint32_t lrbc = lm > 9 ? lm - 9 : 0;
   if (lrbc < lrb) lrbc = lrb;
-  if (lrbc + pb > 31) lrbc = 31 - pb;
-  if (lrbc - lrb > 3) lrbc = lrb + 3;  // F2 <= 8
+  if (lrbc - lrb > ceil_log2(kMaxF2)) return pl;
   const uint64_t R1 = (m + (1ull << lrbc) - 1) >> lrbc;
   if (R1 > (uint64_t)kRMaxCoarse) return pl;
+  const uint32_t ish = pb + lrbc + 1;
+  if (ish > 62) return pl;
+  // keys per run: the index field (all-ones is the filler), 32-bit miss-entry
+  // indices, and < 2^32 record slots over the coarse bins (dual query records)
+  const uint64_t per_rec = op == CKF_OP_QUERY ? 2 : 1;
+  uint64_t kmax = (1ull << (64 - ish)) - 2;
+  if (kmax > (1ull << 31) / per_rec) kmax = (1ull << 31) / per_rec;
+  const uint64_t kenv = env_u64("CKF_MAX_RUN_KEYS", 0);  // developer knob: exercise multi-run calls
+  if (kenv && kenv < kmax) kmax = kenv;
+  const uint64_t runs = (n + kmax - 1) / kmax;
+  pl.chunk = (n + runs - 1) / runs;
   pl.lrb = lrb;
   pl.lrbc = lrbc;
   pl.F2 = 1u << (lrbc - lrb);
   pl.R1 = (uint32_t)R1;
   pl.R = pl.R1 * pl.F2;
   pl.pb = pb;
-  const double recs = (double)n * (op == CKF_OP_QUERY ? 2.0 : 1.0);  // dual query records
+  pl.ish = ish;
+  const double recs = (double)pl.chunk * (double)per_rec;
   // + run padding: at most one filler per bin per tile of the pass that fills it
-  // (bin: ceil(n / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
-  const uint64_t tiles1 = (n + kBTile - 1) / kBTile + (uint64_t)kMaxProbeGrid;
+  // (bin: ceil(chunk / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
+  const uint64_t tiles1 = (pl.chunk + kBTile - 1) / kBTile + (uint64_t)kMaxProbeGrid;
   pl.cap1 = (even_cap(recs / pl.R1) + tiles1 + 1) & ~1ull;
   pl.capf = (even_cap(recs / pl.R) + (pl.cap1 + kBTile - 1) / kBTile + 1) & ~1ull;
+  if ((uint64_t)pl.R1 * pl.cap1 >= 0xFFFFFFFFull) return pl;  // coalesced bin writer: 32-bit slots
   ok = true;
   return pl;
 }
-
 
 // one persistent probe CTA per SM (fewer if there are fewer regions)
 static uint32_t probe_grid(const RPlan& pl) {
@@ -561,7 +467,7 @@ static uint64_t miss_seg(const RPlan& pl) {
   return (uint64_t)((pl.R + gsz - 1) / gsz) * pl.capf;
 }
 
-static RLayout rlayout_for(const RPlan& pl, uint64_t n, int op) {
+static RLayout rlayout_for(const RPlan& pl, int op) {
   RLayout L{};
   const uint64_t cs = (uint64_t)kCntStride * 4;
   L.cnt1 = 0;
@@ -570,12 +476,13 @@ static RLayout rlayout_for(const RPlan& pl, uint64_t n, int op) {
   L.n_miss = L.bin_ctr_end;
   L.mode = L.n_miss + 4ull * kMaxProbeGrid;
   L.ctr_end = align256(L.mode + 8);
-  L.bin1 = L.ctr_end;
+  L.qstart = L.ctr_end;  // insert: eviction-queue length before this run (not zeroed per run)
+  L.room = align256(L.qstart + 8);  // insert: room bit per bucket
+  L.bin1 = align256(L.room + (op == CKF_OP_INSERT ? ((uint64_t)pl.R << pl.lrb) / 8 : 0));
   L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
   L.miss = align256(L.binf + pl.R * pl.capf * 8);
   L.bits = align256(L.miss + probe_grid(pl) * miss_seg(pl) * 16);
-  L.total = align256(L.bits + (op == CKF_OP_INSERT ? 0 : (n + 31) / 32 * 4));
-  (void)op;
+  L.total = align256(L.bits + (op == CKF_OP_INSERT ? 0 : (pl.chunk + 31) / 32 * 4));
   return L;
 }
 
@@ -590,6 +497,7 @@ static RWork rwork_view(void* ws, const RLayout& L, const RPlan& pl) {
   w.binf = (uint64_t*)(b + L.binf);
   w.miss = (uint4*)(b + L.miss);
   w.bits = (uint32_t*)(b + L.bits);
+  w.room = (uint32_t*)(b + L.room);
   w.seg = miss_seg(pl);
   return w;
 }
@@ -607,8 +515,9 @@ static void allow_big_smem(uint32_t bytes) {
   }
 }
 
-// Region run of one op: bin, split, probe on the primary buckets; bin, split,
-// probe the misses on their alternate buckets; (+ bit expansion).
+// Region run of one op over n <= pl.chunk keys: bin, split, probe on the
+// primary buckets; bin, split, probe the misses on their alternate buckets;
+// (+ bit expansion).
 template <int OP, int F, int WPB, int POL>
 static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws, uint64_t* words,
                       const uint64_t* keys, uint64_t n, bool hashed, Sink sk, long long* occ, uint8_t* out,
@@ -665,14 +574,18 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
 }
 
 struct TiledArgs {
-  bool on;      // L2-tiled schedule (ckf_tiled.cuh)
   bool region;  // shared-memory region schedule (ckf_region.cuh)
-  Plan pl;
-  Layout L;
   RPlan rpl;
   RLayout RL;
   void* ws;
 };
+
+// the call's keys in runs of at most pl.chunk: (offset, count) of run k
+static inline uint64_t run_count(const TiledArgs& t, uint64_t n) { return (n + t.rpl.chunk - 1) / t.rpl.chunk; }
+static inline void run_span(const TiledArgs& t, uint64_t n, uint64_t k, uint64_t& off, uint64_t& cnt) {
+  off = k * t.rpl.chunk;
+  cnt = n - off < t.rpl.chunk ? n - off : t.rpl.chunk;
+}
 
 struct QueryArgs {
   Geo g;
@@ -691,14 +604,15 @@ struct QueryOp {
   static int run(const QueryArgs& a) {
     if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
-        return run_region<OP_QUERY, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
-                                                 a.n, a.hashed, sk, nullptr, a.out, a.s);
-      }
-      if (a.t.on) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
-        return run_tiled<OP_QUERY, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, const_cast<uint64_t*>(a.words), a.keys,
-                                                a.n, a.hashed, sk, nullptr, a.out, a.s);
+        for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
+          uint64_t off, cnt;
+          run_span(a.t, a.n, k, off, cnt);
+          Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false, off};
+          const int st = run_region<OP_QUERY, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, const_cast<uint64_t*>(a.words),
+                                                           a.keys + off, cnt, a.hashed, sk, nullptr, a.out + off, a.s);
+          if (st) return st;
+        }
+        return CKF_OK;
       }
     }
     constexpr int KPT = WPB >= 8 ? 1 : (WPB > 0 ? 2 : 1);
@@ -727,6 +641,17 @@ struct InsertArgs {
 };
 
 template <int F, int WPB, int POL>
+static int launch_evict(const InsertArgs& a, uint64_t off, const unsigned long long* qstart, RoomMap rm) {
+  // the queue length is only known on the device: a fixed full-residency grid
+  // strides over it (empty queues exit immediately)
+  const unsigned egrid = (unsigned)sm_count() * kEvictBlocks;
+  evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok + off, a.ev ? a.ev + off : nullptr,
+                                                       a.lost ? a.lost + off : nullptr, a.rec, a.cap, a.ctr, a.occ,
+                                                       a.keys + off, a.hashed, off, qstart, rm);
+  return status();
+}
+
+template <int F, int WPB, int POL>
 struct InsertOp {
   static int run(const InsertArgs& a) {
     if (a.sequential) {
@@ -734,46 +659,36 @@ struct InsertOp {
                                                    a.occ, a.hashed);
       return status();
     }
-    int st = CKF_OK;
-    bool tiled = false;
     if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region && a.cap) {
-        tiled = true;
-        if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
-        if (a.ev && cudaMemsetAsync(a.ev, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
-        if (a.lost && cudaMemsetAsync(a.lost, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
-        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, nullptr, false};
-        st = run_region<OP_INSERT, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
-                                                a.occ, nullptr, a.s);
-        if (st) return st;
-      } else if (a.t.on && a.cap) {
-        tiled = true;
         // every key counts as stored until the eviction pass says otherwise
         if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
         if (a.ev && cudaMemsetAsync(a.ev, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
         if (a.lost && cudaMemsetAsync(a.lost, 0, a.n * 8, a.s) != cudaSuccess) return cuda_error();
-        Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok, nullptr, false};
-        st = run_tiled<OP_INSERT, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk, a.occ,
-                                               nullptr, a.s);
-        if (st) return st;
+        unsigned long long* qstart = (unsigned long long*)((char*)a.t.ws + a.t.RL.qstart);
+        for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
+          uint64_t off, cnt;
+          run_span(a.t, a.n, k, off, cnt);
+          // this run's eviction queue starts where the previous runs' ended
+          if (cudaMemcpyAsync(qstart, &a.ctr->n_queued, 8, cudaMemcpyDeviceToDevice, a.s) != cudaSuccess)
+            return cuda_error();
+          Sink sk{nullptr, a.rec, a.cap, a.ctr, a.ok + off, nullptr, false, off};
+          int st = run_region<OP_INSERT, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys + off, cnt, a.hashed,
+                                                      sk, a.occ, nullptr, a.s);
+          if (st) return st;
+          const RWork w = rwork_view(a.t.ws, a.t.RL, a.t.rpl);
+          const RoomMap rm{getenv("CKF_NO_ROOM_MAP") ? nullptr : w.room};
+          if ((st = launch_evict<F, WPB, POL>(a, off, qstart, rm))) return st;
+        }
+        return CKF_OK;
       }
     }
-    if (!tiled) {
-      unsigned grid = grid_for(a.n, kBlock, 16);
-      insert_kernel<F, WPB, POL><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec,
-                                                           a.cap, a.ctr, a.occ, a.hashed);
-      st = status();
-      if (st) return st;
-    }
-    if (a.cap) {
-      // the queue length is only known on the device: a fixed full-residency grid
-      // strides over it (empty queues exit immediately)
-      unsigned egrid = (unsigned)sm_count() * 4;
-      evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ,
-                                                         a.keys, a.hashed);
-      st = status();
-    }
-    return st;
+    unsigned grid = grid_for(a.n, kBlock, 16);
+    insert_kernel<F, WPB, POL><<<grid, kBlock, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.ok, a.ev, a.lost, a.rec,
+                                                         a.cap, a.ctr, a.occ, a.hashed);
+    int st = status();
+    if (st) return st;
+    return a.cap ? launch_evict<F, WPB, POL>(a, 0, nullptr, RoomMap{nullptr}) : CKF_OK;
   }
 };
 
@@ -800,14 +715,15 @@ struct DeleteOp {
     }
     if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
-        return run_region<OP_DELETE, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
-                                                  a.occ, a.out, a.s);
-      }
-      if (a.t.on) {
-        Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false};
-        return run_tiled<OP_DELETE, F, WPB, POL>(a.g, a.t.pl, a.t.L, a.t.ws, a.words, a.keys, a.n, a.hashed, sk,
-                                                 a.occ, a.out, a.s);
+        for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
+          uint64_t off, cnt;
+          run_span(a.t, a.n, k, off, cnt);
+          Sink sk{nullptr, nullptr, 0, a.ctr, nullptr, nullptr, false, off};
+          const int st = run_region<OP_DELETE, F, WPB, POL>(a.g, a.t.rpl, a.t.RL, a.t.ws, a.words, a.keys + off, cnt,
+                                                            a.hashed, sk, a.occ, a.out + off, a.s);
+          if (st) return st;
+        }
+        return CKF_OK;
       }
     }
     unsigned grid = grid_for(a.n, kBlock, 16);
@@ -1163,47 +1079,54 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
                             (cudaStream_t)stream);
 }
 
-// Decide tiled vs direct for one call: tiled needs the plan to apply and a
-// large enough caller workspace.
-// Developer knob: CKF_SCHED=l2 selects the L2-tiled schedule instead of the
-// shared-memory region schedule (both are legal concurrent schedules).
-static bool use_region() {
-  const char* v = getenv("CKF_SCHED");
-  return !(v && v[0] == 'l');
+// Schedule of one call: the region schedule when its plan applies and the
+// caller's workspace holds it, else the direct kernels.  Automatic choice:
+// tables past the L2 (>= 48 MiB) and at least one key per bucket.
+static bool region_wanted(const ckf_params* p, uint64_t n, unsigned flags) {
+  if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
+  if (n == 0) return false;
+  if (!(flags & CKF_FORCE_TILED)) {
+    if (!env_u64("CKF_TILED_AUTO", 1)) return false;
+    const uint64_t table = p->bucket_count * p->words_per_bucket * 8ull;
+    if (table < kRegionMinTable || n < p->bucket_count) return false;
+  }
+  return true;
 }
 
 static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys, void* ws,
                         uint64_t ws_bytes) {
   TiledArgs t{};
-  if (!ws || !tiled_applies(p, n, flags)) return t;
-  t.ws = ws;
+  if (!ws || !region_wanted(p, n, flags) || ((uintptr_t)keys % 8) != 0 || ((uintptr_t)ws % 256) != 0) return t;
   bool ok = false;
-  if (use_region() && ((uintptr_t)keys % 8) == 0) {
-    t.rpl = make_rplan(p, n, op, flags, ok);
-    if (ok) {
-      t.RL = rlayout_for(t.rpl, n, op);
-      t.region = ws_bytes >= t.RL.total && ((uintptr_t)ws % 256) == 0;
-      if (t.region) return t;
-    }
-  }
-  t.pl = make_plan(p, n, flags, ok);
-  t.L = layout_for(t.pl, n, op);
-  t.on = ws_bytes >= t.L.total && ((uintptr_t)ws % 256) == 0;
+  t.rpl = make_rplan(p, n, op, flags, ok);
+  if (!ok) return t;
+  t.RL = rlayout_for(t.rpl, op);
+  t.ws = ws;
+  t.region = ws_bytes >= t.RL.total;
   return t;
 }
 
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
-  if (!params_ok(p) || !tiled_applies(p, n, flags)) return 0;
-  bool ok;
-  uint64_t need = layout_for(make_plan(p, n, flags, ok), n, op).total;
-  if (use_region()) {
-    const RPlan rp = make_rplan(p, n, op, flags, ok);
-    if (ok) {
-      const uint64_t r = rlayout_for(rp, n, op).total;
-      if (r > need) need = r;
-    }
+  if (!params_ok(p) || !region_wanted(p, n, flags)) return 0;
+  if (op == CKF_OP_INSERT || op == CKF_OP_DELETE || op == CKF_OP_QUERY) {
+    const uint32_t f = p->fingerprint_bits, wpb = p->words_per_bucket;
+    if (f == 32 || (wpb != 2 && wpb != 4 && wpb != 8)) return 0;
   }
-  return need;
+  bool ok;
+  const RPlan rp = make_rplan(p, n, op, flags, ok);
+  return ok ? rlayout_for(rp, op).total : 0;
+}
+
+int ckf_schedule(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys, const void* workspace,
+                 uint64_t workspace_bytes, uint64_t* runs) {
+  if (runs) *runs = 0;
+  if (!params_ok(p)) return CKF_EINVAL;
+  if (flags & CKF_MODE_SEQUENTIAL) return op == CKF_OP_QUERY ? CKF_SCHED_DIRECT : CKF_SCHED_SEQUENTIAL;
+  if (ckf_workspace_bytes(p, n, op, flags) == 0) return CKF_SCHED_DIRECT;
+  const TiledArgs t = choose(p, n, op, flags, keys, const_cast<void*>(workspace), workspace_bytes);
+  if (!t.region) return CKF_SCHED_DIRECT;
+  if (runs) *runs = run_count(t, n);
+  return CKF_SCHED_REGION;
 }
 
 int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint64_t n, uint8_t* ok, int64_t* evictions,
@@ -1295,6 +1218,15 @@ int ckf_kmers(const uint8_t* seq, uint64_t len, uint32_t k, uint64_t* out, unsig
   if ((st = status())) return st;
   kmer_chunk_kernel<true><<<grid, 256, 0, s>>>(seq, len, k, nullptr, offs, out);
   return status();
+}
+
+int ckf_debug_fault_origin_cas(unsigned int count) {
+  return cudaMemcpyToSymbol(g_fault_origin_cas, &count, sizeof(count)) == cudaSuccess ? CKF_OK : cuda_error();
+}
+
+int ckf_debug_faults_pending(unsigned int* count) {
+  if (!count) return CKF_EINVAL;
+  return cudaMemcpyFromSymbol(count, g_fault_origin_cas, sizeof(*count)) == cudaSuccess ? CKF_OK : cuda_error();
 }
 
 uint64_t ckf_host_hash(uint64_t key, uint64_t seed) { return xxh64(key, seed); }

@@ -29,7 +29,7 @@
 
 #include <type_traits>
 
-#include "ckf_tiled.cuh"
+#include "ckf_ops.cuh"
 
 namespace ckf {
 
@@ -259,7 +259,9 @@ __device__ __forceinline__ void clear_bit(uint32_t* bits, uint32_t i) { atomicAn
 constexpr int kRegionSmem = 128 * 1024;  // table bytes of one fine region in shared memory
 constexpr int kRMaxCoarse = 512;
 
-// Record (8 B): index:32 | alt:1 | bucket offset in its region << pb | fp.
+// Record (8 B): index << ish | alt << (ish - 1) | bucket offset in its region << pb | fp,
+// ish = pb + lrbc + 1: the index takes whatever the offset and fingerprint leave
+// (64 - ish >= ceil_log2(chunk + 1) bits; the host chunks larger batches).
 // `alt` marks a record of the key's alternate bucket.
 struct RPlan {
   uint64_t cap1;     // record slots per coarse bin (even)
@@ -270,11 +272,15 @@ struct RPlan {
   uint32_t lrb;      // log2 buckets per fine region
   uint32_t R;        // fine regions = R1 * F2 (the last ones may be empty)
   uint32_t pb;       // fingerprint bits in a record
+  uint32_t ish;      // index shift: pb + lrbc + 1
+  uint64_t chunk;    // keys per region run (a call of n > chunk keys runs ceil(n / chunk) of them)
 };
 
-__device__ __forceinline__ uint64_t rpack(uint64_t idx, uint32_t alt, uint64_t off, uint64_t fp, uint32_t pb) {
-  return (idx << 32) | ((uint64_t)alt << 31) | (off << pb) | fp;
+__device__ __forceinline__ uint64_t rpack(uint64_t idx, uint32_t alt, uint64_t off, uint64_t fp, const RPlan& pl) {
+  return (idx << pl.ish) | ((uint64_t)alt << (pl.ish - 1)) | (off << pl.pb) | fp;
 }
+__device__ __forceinline__ uint32_t ridx(uint64_t rc, uint32_t ish) { return (uint32_t)(rc >> ish); }
+__device__ __forceinline__ uint32_t ralt(uint64_t rc, uint32_t ish) { return (uint32_t)(rc >> (ish - 1)) & 1u; }
 
 struct RWork {
   uint32_t* cnt1;   // [R1 * kCntStride] coarse bin fill
@@ -288,19 +294,20 @@ struct RWork {
   uint32_t* mode;   // [2] mode[0] nonzero: results start all-true and final negatives clear their bit;
                     // zero: results start all-false and hits set theirs (query batches
                     // sampled as mostly negative)
+  uint32_t* room;   // insert: [m/32] bit i = bucket i has an empty lane (RoomMap, ckf_device.cuh)
 };
 
 // What to do with a record that finds its bin full (adversarial inputs only):
 // resolve it in place on the global table -- legal here because no region is
 // resident in shared memory while the bin / split kernels run.
 template <int OP, int F, int WPB, int POL>
-__device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, uint64_t rec, uint64_t bucket,
-                                               const Sink& sk, const uint32_t* w_mode, uint32_t& n_ok,
-                                               uint32_t& n_alt) {
+__device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, uint32_t ish, uint64_t rec,
+                                               uint64_t bucket, const Sink& sk, const uint32_t* w_mode,
+                                               uint32_t& n_ok, uint32_t& n_alt) {
   using Lg = Logic<OP, F, WPB, POL>;
-  const uint32_t idx = (uint32_t)(rec >> 32);
+  const uint32_t idx = ridx(rec, ish);
   const uint64_t fp = rec & ((1ull << g.payload_bits) - 1u);
-  const bool phase2 = (rec >> 31) & 1u;  // the record is of the key's alternate bucket
+  const bool phase2 = ralt(rec, ish);  // the record is of the key's alternate bucket
   uint64_t c;
   bool done;
   if (phase2) {
@@ -332,10 +339,11 @@ constexpr int kBThreads = 256;
 constexpr int kBItems = 16;
 constexpr int kBTile = kBThreads * kBItems;  // records per tile
 // Runs go out as TMA bulk copies, which need 16 B granules: a run of odd
-// length is padded with one filler record (index 0xFFFFFFFF, never a key:
-// batches hold < 2^32 - 1 keys) that every consumer skips.
+// length is padded with one filler record (all ones: its index field would be
+// 2^(64-ish) - 1, never a key, as a run holds < 2^(64-ish) - 1 keys) that every
+// consumer skips.
 constexpr uint64_t kFiller = ~0ull;
-__device__ __forceinline__ bool is_filler(uint64_t rc) { return (uint32_t)(rc >> 32) == 0xFFFFFFFFu; }
+__device__ __forceinline__ bool is_filler(uint64_t rc) { return rc == kFiller; }
 
 struct BinSmem {
   uint64_t rec[kBTile + kRMaxCoarse];  // sorted tile (bulk writer: runs padded to even length)
@@ -524,13 +532,13 @@ __global__ void __launch_bounds__(kBThreads, 3)
         const uint64_t fp = fp0 ? fp0 : 1u;
         const uint64_t i1 = reduce_index(h & 0xFFFFFFFFull, g);
         const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
-        rec[q] = rpack(i, 0u, i1 & lmask, fp, pl.pb);
+        rec[q] = rpack(i, 0u, i1 & lmask, fp, pl);
         pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
         if (q < kBItems / 2 && dual) {
           uint64_t cc;
           const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, cc);
           const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
-          rec[q + kBItems / 2] = rpack(i, 1u, i2 & lmask, fp, pl.pb);
+          rec[q + kBItems / 2] = rpack(i, 1u, i2 & lmask, fp, pl);
           pk[q + kBItems / 2] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
       }
@@ -549,7 +557,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
           const uint64_t i = t0 + (uint64_t)(q0 + q) * kBThreads + threadIdx.x;
           const uint64_t i2 = (uint64_t)e[q].z | ((uint64_t)e[q].w << 32);
           const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
-          rec[q0 + q] = rpack(e[q].x, 1u, i2 & lmask, e[q].y, pl.pb);
+          rec[q0 + q] = rpack(e[q].x, 1u, i2 & lmask, e[q].y, pl);
           pk[q0 + q] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
       }
@@ -563,7 +571,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       if (pk[q] != 0xFFFFFFFFu) bin_place<kBulk>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
     auto ovf = [&](uint64_t rc, uint32_t b) {
       const uint64_t bucket = ((uint64_t)b << pl.lrbc) + ((rc >> pl.pb) & lmask);
-      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
+      resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
     if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
     else bin_write_coalesced(pl.R1, (uint32_t)(min(KT, n - t0) * (dual ? 2 : 1)), w.bin1, pl.cap1, sm, pol, ovf);
@@ -628,7 +636,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       if (pk[q] != 0xFFFFFFFFu) bin_place<true>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
     bin_write(pl.F2, w.binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](uint64_t rc, uint32_t f) {
       const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
-      resolve_direct<OP, F, WPB, POL>(words, g, rc, bucket, sk, w.mode, n_ok, n_alt);
+      resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
     });
     __syncthreads();
   }
@@ -662,7 +670,8 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;
 constexpr uint64_t kRehash = ~0ull;
 
 template <int K>
-__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K]) {
+__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K],
+                                                    uint32_t ish) {
   const int lane = threadIdx.x & 31;
   const uint32_t c = __popc(nm);
   uint32_t incl = c;
@@ -680,8 +689,8 @@ __device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm,
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     if (!((nm >> q) & 1u)) continue;
-    const uint32_t idx = (uint32_t)(rc[q] >> 32);
-    if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{idx, kRehash, 0u, 0u};
+    const uint32_t idx = ridx(rc[q], ish);
+    if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{sk.ibase + idx, kRehash, 0u, 0u};
     else if (sk.ok) sk.ok[idx] = 0;
     ++pos;
   }
@@ -757,8 +766,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
     const uint64_t fpmask = (1ull << pl.pb) - 1u;
     const uint32_t tab_a = saddr(tab);
     const uint64_t pol = evict_first_policy();
-    auto next_region = [&](uint32_t r) -> uint32_t {  // next region of this CTA with records
-      while (r < pl.R && region_count(r) == 0) r += gridDim.x;
+    // next region of this CTA with records (insert phase 1: every region, so
+    // the room map covers the table)
+    constexpr bool kVisitAll = OP == OP_INSERT && PHASE == 1;
+    auto next_region = [&](uint32_t r) -> uint32_t {
+      if (!kVisitAll)
+        while (r < pl.R && region_count(r) == 0) r += gridDim.x;
       return r;
     };
     auto load_table = [&](uint32_t r) {  // consumer thread 0
@@ -805,13 +818,13 @@ __global__ void __launch_bounds__(kPThreads, 1)
             if (!((vm >> q) & 1u)) continue;
             const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
             const uint64_t fp = rc[q] & fpmask;
-            const uint32_t idx = (uint32_t)(rc[q] >> 32);
+            const uint32_t idx = ridx(rc[q], pl.ish);
             if constexpr (OP == OP_QUERY) {
               const bool hit = match_any<F, WPB, POL>(wv[q], fp);
               if (hit && !dflt) set_bit(sk.bits, idx);
               if (PHASE == 2 && !hit && dflt) clear_bit(sk.bits, idx);  // a final negative
               if (PHASE == 1 && !hit && !dflt) {  // dual records: the i2 record is binned already
-                n_alt += !((rc[q] >> 31) & 1u);
+                n_alt += !ralt(rc[q], pl.ish);
               } else if (PHASE == 1 && !hit) {
                 nm |= 1u << q;
                 uint64_t cc;
@@ -854,11 +867,11 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
               for (int q = 0; q < K; ++q)
                 if ((nm >> q) & 1u)
-                  *dst++ = make_uint4((uint32_t)(rc[q] >> 32), (uint32_t)(rc[q] & fpmask), (uint32_t)i2[q],
+                  *dst++ = make_uint4(ridx(rc[q], pl.ish), (uint32_t)(rc[q] & fpmask), (uint32_t)i2[q],
                                       (uint32_t)(i2[q] >> 32));
             }
           } else if constexpr (OP == OP_INSERT && PHASE == 2) {
-            enqueue_evict_batch<K>(sk, nm, rc);
+            enqueue_evict_batch<K>(sk, nm, rc, pl.ish);
           }
         }
         __syncwarp();
@@ -867,9 +880,37 @@ __global__ void __launch_bounds__(kPThreads, 1)
       // region boundary: write the slice back, bring in the next one
       if (kMut) fence_async_smem();  // this thread's shared-memory CASes before the bulk copy
       consumers_sync();
+      if constexpr (OP == OP_INSERT) {
+        // room bit per bucket for the eviction pass (RoomMap): read from the
+        // final shared-memory copy, one ballot word per 32 buckets (phase 1
+        // visits every region, so the map covers the whole table)
+        const uint32_t nb = region_buckets(r);
+        for (uint32_t k0 = warp * 32; k0 < nb; k0 += kPWarps * 32) {
+          const uint32_t k = k0 + lane;
+          bool room = false;
+          if (k < nb) {
+            uint64_t wv[WPB];
+            lds_bucket<WPB>(tab_a + k * bbytes, wv);
+#pragma unroll
+            for (int j = 0; j < WPB; ++j) room |= Lanes<F>::zeros(wv[j]) != 0;
+          }
+          const unsigned bal = __ballot_sync(0xffffffffu, room);
+          if (lane == 0) {
+            const uint64_t b = b0 + k0;
+            if (rb >= 32) {
+              w.room[b >> 5] = bal;
+            } else {  // several regions share a word (small forced tables)
+              const uint32_t msk = (uint32_t)(((1ull << nb) - 1u) << (b & 31));
+              atomicAnd(w.room + (b >> 5), ~msk);
+              atomicOr(w.room + (b >> 5), bal << (b & 31));
+            }
+          }
+        }
+        consumers_sync();  // the slice is read before it is overwritten
+      }
       const uint32_t rn = next_region(r + gridDim.x);
       if (tid == 0) {
-        if (kMut) {
+        if (kMut && cn) {
           bulk_s2g(words + b0 * WPB, tab, region_buckets(r) * bbytes);
           bulk_wait_read();  // the slice has left shared memory
         }

@@ -233,9 +233,10 @@ class CuckooFilter:
             raise RuntimeError("CuckooFilter runs on CUDA devices only")
         self._params = cfg.ckf_params()
         self._deterministic = deterministic
-        # None: library heuristic; True: L2-tiled whenever applicable; False: direct kernels
+        # None: library heuristic; True: region schedule whenever its plan applies; False: direct kernels
         self._tiled_flags = {None: 0, True: _lib.FORCE_TILED, False: _lib.FORCE_DIRECT}[tiled]
-        self._ws = None  # grow-only scratch for the L2-tiled path
+        self._ws = {}  # grow-only region-schedule scratch, one per CUDA stream
+        self.last_schedule = None  # (schedule name, region runs) of the last batch call
         self._pipe = None  # streams + chunk buffers of the host pipeline
         with torch.cuda.device(self.device):
             self.words_device = torch.zeros(cfg.total_words, dtype=torch.int64, device=self.device)
@@ -350,14 +351,36 @@ class CuckooFilter:
         return (_lib.MODE_SEQUENTIAL if det else _lib.MODE_CONCURRENT) | self._tiled_flags
 
     def _workspace(self, p, n: int, op: int, flags: int):
-        """(pointer, bytes) of scratch for an L2-tiled run, or (None, 0)."""
+        """(pointer, bytes) of region-schedule scratch on the current stream, or
+        (None, 0).  One grow-only buffer per stream: batches on different
+        streams never share bins or result bitmaps, and a buffer is only freed
+        after the work queued on its stream."""
         need = int(_lib.lib().ckf_workspace_bytes(ctypes.byref(p), n, op, flags))
         if need == 0:
             return None, 0
-        if self._ws is None or self._ws.numel() < need:
-            self._ws = None
-            self._ws = torch.empty(need, dtype=torch.uint8, device=self.device)
-        return self._ws.data_ptr(), self._ws.numel()
+        s = self._stream()
+        ws = self._ws.get(s)
+        if ws is None or ws.numel() < need:
+            if ws is not None:
+                ws.record_stream(torch.cuda.current_stream(self.device))
+            ws = self._ws[s] = None
+            ws = self._ws[s] = torch.empty(need, dtype=torch.uint8, device=self.device)
+        return ws.data_ptr(), ws.numel()
+
+    def schedule(self, n: int, op: str = "insert", deterministic: Optional[bool] = None):
+        """(schedule, runs) a batch of n device keys would run: "region" (binned,
+        shared-memory probe; `runs` back-to-back region runs), "direct" or
+        "sequential"."""
+        code = {"query": _lib.OP_QUERY, "insert": _lib.OP_INSERT, "delete": _lib.OP_DELETE}[op]
+        flags = self._flags(deterministic) if code != _lib.OP_QUERY else self._tiled_flags
+        return self._schedule_of(self._params, n, code, flags, 0, *self._workspace(self._params, n, code, flags))
+
+    @staticmethod
+    def _schedule_of(p, n: int, op: int, flags: int, kptr: int, ws, wsb):
+        runs = ctypes.c_uint64(0)
+        sc = _lib.lib().ckf_schedule(ctypes.byref(p), n, op, flags, kptr, ws, wsb, ctypes.byref(runs))
+        _lib.check(min(sc, 0))
+        return _lib.SCHED_NAMES[sc], int(runs.value)
 
     def _params_for(self, worker: int):
         if worker == 0:
@@ -445,6 +468,7 @@ class CuckooFilter:
         p = self._params if p is None else p
         L = _lib.lib()
         ws, wsb = self._workspace(p, n, op, flags)
+        self.last_schedule = self._schedule_of(p, n, op, flags, k.data_ptr(), ws, wsb)
         if op == _lib.OP_INSERT:
             _lib.check(L.ckf_insert(
                 ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, out.data_ptr(),

