@@ -12,8 +12,10 @@ the "sequence before the first header" error) into one byte buffer -- each
 record's sequence lines concatenated, one separator byte between records --
 and the window packing runs on the device (``ckf_kmers`` in include/ckf.h:
 a count pass, a scan and an emit pass over 1024-base chunks).
-``stream_kmers`` returns a numpy array (iterating it yields the reference's
-stream); ``as_tensor=True`` keeps the keys on the GPU for ``insert_batch``.
+``stream_kmers`` is the reference's lazy iterator of ints (the device packs
+the whole source at the first ``next``); ``kmer_array`` returns the same
+stream as one numpy uint64 array and ``stream_kmers(..., as_tensor=True)`` as
+the device tensor ``insert_batch`` takes.
 """
 
 from __future__ import annotations
@@ -99,17 +101,29 @@ def kmers_from_buffer(buf, k: int, device=None) -> torch.Tensor:
         return out[: int(n_out.item())]
 
 
-def stream_kmers(source, k: int, *, as_tensor: bool = False, device=None):
-    """Every valid k-mer window of a FASTA source, packed (kmer.py:77-95).
-
-    ``source`` is a path or an iterable of lines.  Returns a numpy uint64
-    array in stream order (or the device tensor with ``as_tensor=True``)."""
+def kmer_array(source, k: int, device=None) -> np.ndarray:
+    """The packed stream of ``stream_kmers`` as one numpy uint64 array."""
     if not 1 <= k <= 31:
         raise ValueError(f"k must be in [1, 31], got {k}")
-    keys = kmers_from_buffer(sequence_buffer(source), k, device)
+    return kmers_from_buffer(sequence_buffer(source), k, device).cpu().numpy().view(np.uint64)
+
+
+def _iter_kmers(source, k: int, device):
+    yield from (int(v) for v in kmer_array(source, k, device))
+
+
+def stream_kmers(source, k: int, *, as_tensor: bool = False, device=None):
+    """Yield every valid k-mer window of a FASTA source, packed (kmer.py:77-95).
+
+    ``source`` is a path or an iterable of lines.  Like the reference, a lazy
+    iterator: k and the FASTA structure are checked when iteration starts.
+    ``as_tensor=True`` (extension) returns the whole stream at once as the
+    device int64 tensor that ``CuckooFilter.insert_batch`` takes."""
     if as_tensor:
-        return keys
-    return keys.cpu().numpy().view(np.uint64)
+        if not 1 <= k <= 31:
+            raise ValueError(f"k must be in [1, 31], got {k}")
+        return kmers_from_buffer(sequence_buffer(source), k, device)
+    return _iter_kmers(source, k, device)
 
 
 def kmer_bench(path, k: int, spec: RunSpec) -> list[BenchReport]:

@@ -8,12 +8,14 @@ record breaks sit on the device's 1024-base chunk boundaries.
 
 from __future__ import annotations
 
+from pathlib import Path
+
 import numpy as np
 import pytest
 
 from paper_2603_15486_b200 import CuckooFilter, FilterConfig
 from paper_2603_15486_b200.bench_harness import RunSpec
-from paper_2603_15486_b200.kmer import kmer_bench, stream_kmers
+from paper_2603_15486_b200.kmer import kmer_array, kmer_bench, stream_kmers
 
 pytestmark = pytest.mark.gpu
 
@@ -123,7 +125,7 @@ def test_long_records_across_chunk_boundaries(k):
         lines.append(f">r{i}")
         lines += [r[j:j + 80] for j in range(0, len(r), 80)]
     want = np.concatenate([fast_naive(r, k) for r in recs])
-    got = stream_kmers(lines, k)
+    got = kmer_array(lines, k)
     assert got.dtype == np.uint64 and np.array_equal(got, want)
 
 
@@ -150,3 +152,19 @@ def test_kmer_bench_reports_three_phases(tmp_path):
     assert [r.op for r in reports] == ["insert", "query_pos", "delete"]
     assert all(r.n_keys == len(seq) - 30 for r in reports)
     assert reports[0].insert_failures == 0 and all(r.throughput > 0 for r in reports)
+
+
+# ---- pinned to the reference's own output (tests/golden/make_kmer_golden.py) ----
+
+@pytest.mark.parametrize("name", ["tiny", "synth"])
+@pytest.mark.parametrize("k", [1, 2, 5, 15, 21, 31])
+def test_stream_matches_reference_golden(name, k):
+    z = np.load(Path(__file__).parent / "golden" / "kmer_golden.npz")
+    text = bytes(z[f"{name}_fasta"]).decode()
+    want = z[f"{name}_k{k}"]
+    got = kmer_array(text.splitlines(keepends=True), k)
+    assert np.array_equal(got, want)
+    if name == "tiny" and k == 31:
+        assert len(got) == 332  # reference pkg/tests/test_cli.py:97
+    it = stream_kmers(text.splitlines(keepends=True), k)
+    assert iter(it) is it and [next(it) for _ in range(min(3, len(want)))] == [int(v) for v in want[:3]]

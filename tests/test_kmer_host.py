@@ -63,7 +63,32 @@ def test_headerless_sequence_raises_with_line_number():
 
 
 def test_stream_k_validation_happens_before_any_device_work():
+    # a lazy iterator like the reference's generator: checked on first next()
+    it = stream_kmers([">r", "ACGT"], 0)
     with pytest.raises(ValueError):
-        stream_kmers([">r", "ACGT"], 0)
+        list(it)
     with pytest.raises(ValueError):
-        stream_kmers([">r", "ACGT"], 32)
+        list(stream_kmers([">r", "ACGT"], 32))
+    with pytest.raises(ValueError):
+        stream_kmers([">r", "ACGT"], 32, as_tensor=True)
+    with pytest.raises(FastaError):
+        list(stream_kmers(["", "  ", "ACGT"], 2))
+
+
+def test_kmer_golden_fixture_is_the_reference_stream():
+    """The fixture's tiny.fasta windows, re-packed on the host with pack_kmer,
+    equal the reference stream stored next to it (pins the fixture itself)."""
+    from pathlib import Path
+
+    z = np.load(Path(__file__).parent / "golden" / "kmer_golden.npz")
+    for name in ("tiny", "synth"):
+        text = bytes(z[f"{name}_fasta"]).decode()
+        for k in (5, 31):
+            want = []
+            for rec in text.split(">")[1:]:
+                seq = "".join(ln.strip() for ln in rec.splitlines()[1:])
+                for i in range(len(seq) - k + 1):
+                    v = pack_kmer(seq[i:i + k])
+                    if v is not None:
+                        want.append(v)
+            assert np.array_equal(np.array(want, dtype=np.uint64), z[f"{name}_k{k}"]), (name, k)
