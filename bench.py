@@ -189,13 +189,23 @@ def host_threads() -> int:
         return os.cpu_count() or 1
 
 
-def workload_config(log2: int, world: int, eviction: str) -> dict:
+def per_gpu_log2(args, world: int) -> int:
+    """Slots per GPU: configs[1]'s 2^28 per GPU (weak scaling), or with
+    --strong configs[3]'s 2^31 in total over the N GPUs."""
+    return args.strong_log2_total - (world.bit_length() - 1) if args.strong else args.log2_slots
+
+
+def workload_config(log2: int, world: int, eviction: str, strong: bool = False) -> dict:
     n = int(0.95 * (1 << log2))
-    return {"workload": "configs[1]: 2^28 slots/GPU f=16 b=16 xor, insert 0->95% then lookup+/-, delete",
+    wl = ("configs[3]: 2^31 slots total, hash-sharded over the GPUs, f=16 b=16 xor, insert 0->95% then "
+          "lookup+/-, delete" if strong else
+          "configs[1]: 2^28 slots/GPU f=16 b=16 xor, insert 0->95% then lookup+/-, delete")
+    return {"workload": wl,
             "slots_per_gpu": 1 << log2, "keys_per_op_per_gpu": n, "fingerprint_bits": 16,
             "bucket_slots": 16, "policy": "xor", "eviction": eviction,
             "parallelism": f"hash-sharded x{world}" if world > 1 else "single GPU",
-            "l2": "inputs > L2 (2 GiB key arrays, 512 MiB table vs 126 MB L2); no flush"}
+            "l2": f"inputs > L2 ({8 * int(0.95 * (1 << log2)) >> 20} MiB key arrays, {(1 << log2) * 2 >> 20} MiB "
+                  "table vs 126 MB L2); no flush"}
 
 
 def run_reference(args) -> None:
@@ -203,9 +213,10 @@ def run_reference(args) -> None:
     if rank != 0:
         return
     threads = host_threads()
-    n = int(0.95 * (1 << args.log2_slots))
+    log2 = per_gpu_log2(args, args.gpus)
+    n = int(0.95 * (1 << log2))
     pos, neg = gen_keys(n, 0), gen_keys(n, 0, negative=True)
-    arm = CpuArm(args.log2_slots, pos, neg, threads)
+    arm = CpuArm(log2, pos, neg, threads)
     for _ in range(args.warmup):
         arm.step()
     runs = [arm.step() for _ in range(args.steps)]
@@ -214,9 +225,9 @@ def run_reference(args) -> None:
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": args.gpus,
         "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * sum(secs) / len(secs),
-        "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
-        "data": "synthetic (reference gen_keys Philox streams)",
-        "config": workload_config(args.log2_slots, args.gpus, args.eviction),
+        "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+        "dtype": "u64", "data": "synthetic (reference gen_keys Philox streams)",
+        "config": workload_config(log2, args.gpus, args.eviction, args.strong),
         "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": "port", "sample": arm.describe(),
                          "cpu": cpu_model()},
         "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
@@ -254,7 +265,7 @@ def run_ours(args) -> None:
     from paper_2603_15486_b200 import CuckooFilter, FilterConfig, _lib
     from paper_2603_15486_b200.sharded import ShardedCuckooFilter
 
-    log2 = args.log2_slots
+    log2 = per_gpu_log2(args, world)
     f, b = 16, 16
     m_local = (1 << log2) // b
     n = int(0.95 * (1 << log2))  # keys per rank per op
@@ -350,7 +361,7 @@ def run_ours(args) -> None:
     dom = max(ops, key=lambda o: per_op[o])
     traffic, kernels = None, None
     tf = ROOT / "profiles" / "traffic.json"
-    if tf.exists():
+    if tf.exists() and log2 == 28:  # (the capture is of the 2^28-slot configuration)
         tj = json.loads(tf.read_text())
         traffic = tj.get(dom)
         kernels = [k[0] for k in tj.get(dom + "_kernels", [])]
@@ -418,9 +429,10 @@ def run_ours(args) -> None:
         line = {
             "metric": METRIC, "value": round(value, 4), "unit": UNIT, "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": round(ms_step, 4),
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "u64",
+            "higher_is_better": True, "scaling": "strong" if args.strong else "weak", "vs_baseline": None,
+            "dtype": "u64",
             "data": "synthetic (reference gen_keys Philox streams, seed = rank)",
-            "config": workload_config(log2, world, args.eviction),
+            "config": workload_config(log2, world, args.eviction, args.strong),
             "roofline": roofline, "ops": op_stats, "verify": verify,
             "cpu_baseline": cpu, "e2e": e2e, "gpu_launches": int(launches),
             "clocks": clk.summary(),
@@ -438,6 +450,9 @@ def main() -> None:
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
     ap.add_argument("--log2-slots", type=int, default=28)
+    ap.add_argument("--strong", action="store_true",
+                    help="configs[3]: fixed 2^31 slots in total over the N GPUs (strong scaling)")
+    ap.add_argument("--strong-log2-total", type=int, default=31)
     ap.add_argument("--eviction", choices=["dfs", "bfs"], default="bfs")
     ap.add_argument("--e2e-steps", type=int, default=5)
     ap.add_argument("--no-e2e", action="store_true")

@@ -84,6 +84,10 @@ typedef struct ckf_params {
   uint32_t policy;            /* CKF_POLICY_* */
   uint32_t eviction;          /* CKF_EVICT_* */
   uint32_t max_evictions;     /* >= 1 */
+  uint32_t shard_shift;       /* sharded filter (ckf_params_set_shard): owner = (h >> shift) & mask */
+  uint32_t shard_mask;        /*   0: not sharded */
+  uint32_t shard_id;          /*   this shard; with CKF_INPUT_HASHED, hashes owned by another */
+  uint32_t shard_reserved;    /*   shard are skipped (padding of the fixed-size exchange) */
 } ckf_params;
 
 /* Sparse per-key insert outcome for keys that needed the eviction path
@@ -117,6 +121,13 @@ uint64_t ckf_kernel_launches(void);
 int ckf_params_init(ckf_params* p, uint64_t bucket_count, uint32_t fingerprint_bits,
                     uint32_t bucket_slots, int policy, int eviction, uint32_t max_evictions,
                     uint64_t seed);
+
+/* Mark p as shard `id` of `shards` (a power of two <= 256) routed by hash bits
+ * [shift, shift + log2 shards): hashed batches then skip every hash owned by
+ * another shard -- the sentinel padding of ckf_route_partition_padded -- with
+ * no effect on the table, the occupancy or the counters (a skipped key's
+ * result is unspecified).  shards == 1 clears it. */
+int ckf_params_set_shard(ckf_params* p, uint32_t shift, uint32_t shards, uint32_t id);
 
 /* out[i] = xxh64(keys[i], seed) */
 int ckf_hash(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, void* stream);
@@ -167,6 +178,23 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
 uint64_t ckf_route_workspace_bytes(uint64_t n, uint32_t shards);
 int ckf_route_partition(const uint64_t* hashes, uint64_t n, uint32_t shift, uint32_t shards, uint64_t* send,
                         long long* order, long long* shard_counts, void* workspace, uint64_t workspace_bytes,
+                        void* stream);
+
+/* Fixed-capacity routing for a host-sync-free exchange: like
+ * ckf_route_partition, but shard s's hashes go to send[s*cap ..) in arrival
+ * order, the rest of its block holds a hash owned by shard (s+1) % shards
+ * (skipped by the receiver, see ckf_params_set_shard) with order[] = -1, and
+ * hashes past `cap` in a shard are not sent: *spilled (device) counts them and
+ * their callers find them unanswered.  send / order: shards * cap entries.
+ * workspace: ckf_route_workspace_bytes(n, shards). */
+int ckf_route_partition_padded(const uint64_t* hashes, uint64_t n, uint32_t shift, uint32_t shards, uint64_t cap,
+                               uint64_t* send, long long* order, long long* shard_counts,
+                               unsigned long long* spilled, void* workspace, uint64_t workspace_bytes, void* stream);
+
+/* out[order[p] * elem] <- back[p * elem] for every p < n with order[p] >= 0
+ * (the return path of the routing: answers back to the caller's order);
+ * elem in {1, 8} bytes. */
+int ckf_route_unpermute(const void* back, const long long* order, uint64_t n, uint32_t elem, void* out,
                         void* stream);
 
 /* k-mer ingestion (replaces swarcuckoo/kmer.py:48-95 stream_kmers' packing

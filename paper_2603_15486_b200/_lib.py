@@ -60,6 +60,10 @@ class Params(ctypes.Structure):
         ("policy", ctypes.c_uint32),
         ("eviction", ctypes.c_uint32),
         ("max_evictions", ctypes.c_uint32),
+        ("shard_shift", ctypes.c_uint32),
+        ("shard_mask", ctypes.c_uint32),
+        ("shard_id", ctypes.c_uint32),
+        ("shard_reserved", ctypes.c_uint32),
     ]
 
 
@@ -86,6 +90,10 @@ SIGNATURES = {
     "ckf_query": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _u64, ctypes.c_uint, _vp]),
     "ckf_delete": (ctypes.c_int, [_P, _vp, _vp, _u64, _vp, _vp, _vp, _vp, _u64, ctypes.c_uint,
                                   _vp]),
+    "ckf_params_set_shard": (ctypes.c_int, [_P, _u32, _u32, _u32]),
+    "ckf_route_partition_padded": (ctypes.c_int, [_vp, _u64, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _vp, _u64,
+                                                  _vp]),
+    "ckf_route_unpermute": (ctypes.c_int, [_vp, _vp, _u64, _u32, _vp, _vp]),
     "ckf_route_workspace_bytes": (_u64, [_u64, _u32]),
     "ckf_route_partition": (ctypes.c_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp, _u64, _vp]),
     "ckf_kmer_workspace_bytes": (_u64, [_u64]),

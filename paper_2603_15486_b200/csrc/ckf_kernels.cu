@@ -84,6 +84,7 @@ __global__ void __launch_bounds__(kBlock) query_kernel(Geo g, const uint64_t* __
       uint64_t i = t0 + k * kBlock + threadIdx.x;
       valid[k] = i < n;
       uint64_t h = valid[k] ? load_hash(keys, i, g.seed, hashed) : 0;
+      if (hashed && foreign(g, h)) valid[k] = false;  // padding of the sharded exchange
       place<POL>(h, g, fp[k], i1[k], i2[k]);
     }
     bool hit[KPT];
@@ -159,8 +160,12 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
     const bool valid = i < n;
     bool need = false;
     uint64_t h = 0, fp = 0, i1 = 0, i2 = 0;
-    if (valid) {
-      h = load_hash(keys, i, g.seed, hashed);
+    if (valid) h = load_hash(keys, i, g.seed, hashed);
+    if (valid && hashed && foreign(g, h)) {  // padding of the sharded exchange
+      ok[i] = 1;
+      if (ev) ev[i] = 0;
+      if (lost) lost[i] = 0;
+    } else if (valid) {
       place<POL>(h, g, fp, i1, i2);
       bool done = try_insert_any<F, WPB>(words, i1, fp, g) >= 0;
       if (!done) {
@@ -238,7 +243,12 @@ __global__ void __launch_bounds__(kBlock) delete_kernel(Geo g, uint64_t* __restr
   uint32_t n_ok = 0, n_alt = 0;
   for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
     uint64_t fp, i1, i2;
-    place<POL>(load_hash(keys, i, g.seed, hashed), g, fp, i1, i2);
+    const uint64_t h = load_hash(keys, i, g.seed, hashed);
+    if (hashed && foreign(g, h)) {  // padding of the sharded exchange
+      out[i] = 0;
+      continue;
+    }
+    place<POL>(h, g, fp, i1, i2);
     bool done = remove_tag_any<F, WPB>(words, i1, fp, g) >= 0;
     if (!done) {
       ++n_alt;
@@ -262,6 +272,12 @@ __global__ void seq_insert_kernel(Geo g, uint64_t* words, const uint64_t* keys, 
     uint64_t fp, i1, i2;
     place<POL>(h, g, fp, i1, i2);
     Outcome o{1u, 0u, 0};
+    if (hashed && foreign(g, h)) {  // padding of the sharded exchange
+      ok[i] = 1;
+      if (ev) ev[i] = 0;
+      if (lost) lost[i] = 0;
+      continue;
+    }
     if (try_insert_any<F, WPB>(words, i1, fp, g) < 0 &&
         try_insert_any<F, WPB>(words, i2, make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g), g) < 0)
       o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
@@ -286,7 +302,12 @@ __global__ void seq_delete_kernel(Geo g, uint64_t* words, const uint64_t* keys, 
   uint64_t n_ok = 0;
   for (uint64_t i = 0; i < n; ++i) {
     uint64_t fp, i1, i2;
-    place<POL>(hashed ? keys[i] : xxh64(keys[i], g.seed), g, fp, i1, i2);
+    const uint64_t h = hashed ? keys[i] : xxh64(keys[i], g.seed);
+    if (hashed && foreign(g, h)) {
+      out[i] = 0;
+      continue;
+    }
+    place<POL>(h, g, fp, i1, i2);
     bool done = remove_tag_rt<F>(words, i1, fp, g) >= 0;
     if (!done) done = remove_tag_rt<F>(words, i2, POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp, g) >= 0;
     out[i] = done;
@@ -786,9 +807,10 @@ __global__ void __launch_bounds__(kRtThreads) route_count_kernel(const uint64_t*
 
 // one block: offs[t * G + s] = base[s] + sum_{t' < t} counts[t' * G + s];
 // shard_counts[s] = total of s.  Shards are scanned one after the other.
+// cap != 0 (fixed-capacity exchange): shard s's run starts at s * cap.
 __global__ void __launch_bounds__(1024) route_scan_kernel(const uint32_t* __restrict__ tile_counts, uint64_t ntiles,
                                                           uint32_t G, uint64_t* __restrict__ offs,
-                                                          long long* __restrict__ shard_counts) {
+                                                          long long* __restrict__ shard_counts, uint64_t cap) {
   __shared__ uint64_t wprefix[32];
   __shared__ uint64_t s_total, s_base;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5, nw = blockDim.x / 32;
@@ -819,7 +841,7 @@ __global__ void __launch_bounds__(1024) route_scan_kernel(const uint32_t* __rest
       if (lane == 31) s_total = t;
     }
     __syncthreads();
-    uint64_t run = s_base + wprefix[wid] + x - sum;
+    uint64_t run = (cap ? s * cap : s_base) + wprefix[wid] + x - sum;
     for (uint64_t t = lo; t < hi; ++t) {
       offs[t * G + s] = run;
       run += tile_counts[t * G + s];
@@ -844,7 +866,8 @@ __global__ void __launch_bounds__(kRtThreads, 2) route_scatter_kernel(const uint
                                                                       uint32_t shift, uint32_t gmask,
                                                                       const uint64_t* __restrict__ offs,
                                                                       uint64_t* __restrict__ send,
-                                                                      long long* __restrict__ order) {
+                                                                      long long* __restrict__ order, uint64_t cap,
+                                                                      unsigned long long* spilled) {
   extern __shared__ __align__(16) uint64_t rsm[];
   uint64_t* hin = rsm;                          // [kRtPad] tile, padded
   uint64_t* hout = rsm + kRtPad;                // [kRtTile] shard-sorted hashes
@@ -921,8 +944,40 @@ __global__ void __launch_bounds__(kRtThreads, 2) route_scatter_kernel(const uint
     for (int k = 1; k < 8; ++k)
       if (p >= s_start[k]) q = k;
     const uint64_t pos = tb[q] + (p - s_start[q]);
+    if (cap && pos - (uint64_t)q * cap >= cap) {  // past the shard's capacity: not sent
+      atomicAdd(spilled, 1ull);
+      continue;
+    }
     send[pos] = hout[p];
     order[pos] = oout[p];
+  }
+}
+
+// Padding of the fixed-capacity exchange: the unused tail of shard s's block
+// gets a hash owned by shard (s+1) % G (skipped by the receiver) and order -1.
+__global__ void __launch_bounds__(256) route_fill_kernel(uint64_t* __restrict__ send, long long* __restrict__ order,
+                                                         const long long* __restrict__ shard_counts, uint32_t G,
+                                                         uint64_t cap, uint32_t shift) {
+  __shared__ uint64_t s_cnt[256];
+  for (uint32_t s = threadIdx.x; s < G; s += blockDim.x) s_cnt[s] = (uint64_t)shard_counts[s];
+  __syncthreads();
+  const uint64_t total = (uint64_t)G * cap;
+  for (uint64_t i = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; i < total; i += (uint64_t)gridDim.x * blockDim.x) {
+    const uint32_t s = (uint32_t)(i / cap);
+    if (i - (uint64_t)s * cap >= s_cnt[s]) {
+      send[i] = (uint64_t)((s + 1) & (G - 1)) << shift;
+      order[i] = -1;
+    }
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(256) route_unpermute_kernel(const T* __restrict__ back,
+                                                              const long long* __restrict__ order, uint64_t n,
+                                                              T* __restrict__ out) {
+  for (uint64_t p = blockIdx.x * (uint64_t)blockDim.x + threadIdx.x; p < n; p += (uint64_t)gridDim.x * blockDim.x) {
+    const long long o = order[p];
+    if (o >= 0) out[o] = back[p];
   }
 }
 
@@ -1189,11 +1244,65 @@ int ckf_route_partition(const uint64_t* hashes, uint64_t n, uint32_t shift, uint
   route_count_kernel<<<(unsigned)nt, kRtThreads, 0, s>>>(hashes, n, shift, gmask, counts);
   int st = status();
   if (st) return st;
-  route_scan_kernel<<<1, 1024, 0, s>>>(counts, nt, shards, offs, shard_counts);
+  route_scan_kernel<<<1, 1024, 0, s>>>(counts, nt, shards, offs, shard_counts, 0);
   if ((st = status())) return st;
   allow_big_smem<route_scatter_kernel>(kRouteSmem);
-  route_scatter_kernel<<<(unsigned)nt, kRtThreads, kRouteSmem, s>>>(hashes, n, shift, gmask, offs, send, order);
+  route_scatter_kernel<<<(unsigned)nt, kRtThreads, kRouteSmem, s>>>(hashes, n, shift, gmask, offs, send, order, 0,
+                                                                   nullptr);
   return status();
+}
+
+int ckf_route_partition_padded(const uint64_t* hashes, uint64_t n, uint32_t shift, uint32_t shards, uint64_t cap,
+                               uint64_t* send, long long* order, long long* shard_counts,
+                               unsigned long long* spilled, void* workspace, uint64_t workspace_bytes, void* stream) {
+  if (shards < 2 || shards > 8 || (shards & (shards - 1)) || shift > 63 || !shard_counts || !spilled || cap == 0)
+    return CKF_EINVAL;
+  if (!send || !order) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(spilled, 0, 8, s) != cudaSuccess) return cuda_error();
+  const uint32_t gmask = shards - 1;
+  int st;
+  if (n == 0) {
+    if (cudaMemsetAsync(shard_counts, 0, 8ull * shards, s) != cudaSuccess) return cuda_error();
+  } else {
+    if (!hashes || !workspace || workspace_bytes < ckf_route_workspace_bytes(n, shards)) return CKF_EINVAL;
+    const uint64_t nt = (n + kRtTile - 1) / kRtTile;
+    if (nt > 0x7FFFFFFFull) return CKF_EINVAL;
+    uint32_t* counts = (uint32_t*)workspace;
+    uint64_t* offs = (uint64_t*)((char*)workspace + align256(nt * shards * 4));
+    route_count_kernel<<<(unsigned)nt, kRtThreads, 0, s>>>(hashes, n, shift, gmask, counts);
+    if ((st = status())) return st;
+    route_scan_kernel<<<1, 1024, 0, s>>>(counts, nt, shards, offs, shard_counts, cap);
+    if ((st = status())) return st;
+    allow_big_smem<route_scatter_kernel>(kRouteSmem);
+    route_scatter_kernel<<<(unsigned)nt, kRtThreads, kRouteSmem, s>>>(hashes, n, shift, gmask, offs, send, order,
+                                                                     cap, spilled);
+    if ((st = status())) return st;
+  }
+  route_fill_kernel<<<grid_for((uint64_t)shards * cap, 256, 8), 256, 0, s>>>(send, order, shard_counts, shards, cap,
+                                                                             shift);
+  return status();
+}
+
+int ckf_route_unpermute(const void* back, const long long* order, uint64_t n, uint32_t elem, void* out,
+                        void* stream) {
+  if (n == 0) return CKF_OK;
+  if (!back || !order || !out || (elem != 1 && elem != 8)) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  const unsigned grid = grid_for(n, 256, 8);
+  if (elem == 1)
+    route_unpermute_kernel<uint8_t><<<grid, 256, 0, s>>>((const uint8_t*)back, order, n, (uint8_t*)out);
+  else
+    route_unpermute_kernel<uint64_t><<<grid, 256, 0, s>>>((const uint64_t*)back, order, n, (uint64_t*)out);
+  return status();
+}
+
+int ckf_params_set_shard(ckf_params* p, uint32_t shift, uint32_t shards, uint32_t id) {
+  if (!p || shards < 1 || shards > 256 || (shards & (shards - 1)) || id >= shards || shift > 63) return CKF_EINVAL;
+  p->shard_shift = shards > 1 ? shift : 0;
+  p->shard_mask = shards - 1;
+  p->shard_id = shards > 1 ? id : 0;
+  return CKF_OK;
 }
 
 uint64_t ckf_kmer_workspace_bytes(uint64_t len) {

@@ -528,18 +528,19 @@ __global__ void __launch_bounds__(kBThreads, 3)
         if (dual && q >= kBItems / 2) continue;  // filled with key q - kBItems/2's i2 record
         const uint64_t i = t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
         const uint64_t h = hashed ? kk[q] : xxh64(kk[q], g.seed);
+        const bool mine = i < n && !(hashed && foreign(g, h));  // (padding of the sharded exchange: skipped)
         const uint64_t fp0 = (h >> 32) & ((1ull << g.payload_bits) - 1u);
         const uint64_t fp = fp0 ? fp0 : 1u;
         const uint64_t i1 = reduce_index(h & 0xFFFFFFFFull, g);
         const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
         rec[q] = rpack(i, 0u, i1 & lmask, fp, pl);
-        pk[q] = i < n ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
+        pk[q] = mine ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
         if (q < kBItems / 2 && dual) {
           uint64_t cc;
           const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, cc);
           const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
           rec[q + kBItems / 2] = rpack(i, 1u, i2 & lmask, fp, pl);
-          pk[q + kBItems / 2] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
+          pk[q + kBItems / 2] = mine ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
       }
     } else {
@@ -941,9 +942,10 @@ __global__ void __launch_bounds__(256) region_sample_kernel(Geo g, const uint64_
   if (k < ns) {
     const uint64_t i = (uint64_t)k * n / ns;
     uint64_t fp, i1, i2;
-    place<POL>(hashed ? keys[i] : xxh64(keys[i], g.seed), g, fp, i1, i2);
+    const uint64_t h = hashed ? keys[i] : xxh64(keys[i], g.seed);
+    place<POL>(h, g, fp, i1, i2);
     uint64_t* w = const_cast<uint64_t*>(words);
-    hit = Lg::first(w, i1, fp, g) || Lg::second(w, i2, fp, g);
+    hit = !(hashed && foreign(g, h)) && (Lg::first(w, i1, fp, g) || Lg::second(w, i2, fp, g));
   }
   const uint32_t c = __popc(__ballot_sync(0xffffffffu, hit));
   if ((threadIdx.x & 31) == 0 && c) atomicAdd(mode + 1, c);

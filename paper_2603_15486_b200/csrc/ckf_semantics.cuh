@@ -68,7 +68,14 @@ CKF_HD uint64_t mulhi64(uint64_t a, uint64_t b) {
 struct Geo {
   uint64_t seed, m, mask, high, choice_bit, magic, worker;
   uint32_t f, b, wpb, tpw, payload_bits, policy, eviction, max_evictions;
+  uint32_t shard_shift, shard_mask, shard_id;
 };
+
+// A hashed key owned by another shard (the padding of the fixed-size
+// multi-GPU exchange): skipped by every kernel.
+CKF_HD bool foreign(const Geo& g, uint64_t h) {
+  return g.shard_mask && (uint32_t)((h >> g.shard_shift) & g.shard_mask) != g.shard_id;
+}
 
 CKF_HD Geo geo_from(const ckf_params& p) {
   Geo g;
@@ -87,6 +94,9 @@ CKF_HD Geo geo_from(const ckf_params& p) {
   g.policy = p.policy;
   g.eviction = p.eviction;
   g.max_evictions = p.max_evictions;
+  g.shard_shift = p.shard_shift;
+  g.shard_mask = p.shard_mask;
+  g.shard_id = p.shard_id;
   return g;
 }
 

@@ -47,7 +47,7 @@ def test_exported_symbols_are_c_linkage():
 
 
 def test_struct_sizes_match_header():
-    assert ctypes.sizeof(_lib.Params) == 7 * 8 + 8 * 4
+    assert ctypes.sizeof(_lib.Params) == 7 * 8 + 12 * 4
     assert _lib.RECORD_BYTES == 24 and _lib.COUNTERS_BYTES == 32
 
 
