@@ -13,8 +13,11 @@ from __future__ import annotations
 import ctypes
 from pathlib import Path
 
+import os
+
 _HERE = Path(__file__).resolve().parent
-LIB_PATH = _HERE / "libckf.so"
+# CKF_LIB: developer override (A/B builds of the same sources); never a fallback
+LIB_PATH = Path(os.environ["CKF_LIB"]) if os.environ.get("CKF_LIB") else _HERE / "libckf.so"
 
 ABI_VERSION = 2
 OK = 0

@@ -234,6 +234,155 @@ __global__ void __launch_bounds__(kBlock, kEvictBlocks) evict_kernel(Geo g, uint
   block_count_add(n_ok, 0, ctr, occ, +1);
 }
 
+// BFS eviction pass of the region schedule, one ROUND at a time per lane.
+// The chains of a warp's 32 queued keys differ in length (at 95 % load: mean
+// 1.11 rounds, mean warp maximum 2.23; profiles/r02_evict_rounds.txt), so
+// evict_kernel's one-chain-per-loop-iteration leaves half the lanes idle.  Here
+// every lane runs one BFS round (K:391-436, the same decisions and PRNG stream
+// as evict_chain_t) per iteration and a lane whose chain ended takes the next
+// queue entry (warp-aggregated cursor), so the warp stays full.  Candidates'
+// room comes from the room map (RoomMap, ckf_device.cuh).
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBlock, kEvictBlocks)
+    evict_bfs_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok, int64_t* __restrict__ ev,
+                     uint64_t* __restrict__ lost, ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                     long long* occ, const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
+                     unsigned long long* cursor, RoomMap rm) {
+  using L = Lanes<F>;
+  constexpr int kTpw = L::kTpw;
+  constexpr uint32_t kB = WPB * kTpw;
+  constexpr uint32_t kLim = kB / 2 ? kB / 2 : 1;
+  constexpr uint64_t kAll = kB == 64 ? ~0ull : ((1ull << kB) - 1u);
+  const unsigned long long queued = *(volatile unsigned long long*)&ctr->n_queued;
+  const uint64_t total = queued < cap ? queued : cap;
+  const int lane = threadIdx.x & 31;
+  uint32_t n_ok = 0;
+  bool have = false, drained = false;
+  uint64_t r = 0, i = 0, st = 0, cur_b = 0, cur_tag = 0;
+  uint32_t n = 0;
+  while (true) {
+    // lanes without a chain take the next queue entries
+    const unsigned need = __ballot_sync(0xffffffffu, !have && !drained);
+    if (need) {
+      unsigned long long base = 0;
+      const int leader = __ffs(need) - 1;
+      if (lane == leader) base = atomicAdd(cursor, (unsigned long long)__popc(need));
+      base = __shfl_sync(0xffffffffu, base, leader);
+      if (!have && !drained) {
+        r = base + __popc(need & ((1u << lane) - 1u));
+        if (r < total) {
+          i = rec[r].index - ibase;
+          uint64_t h = rec[r].lost;  // the key hash parked by the queueing pass, or kRehash
+          if (h == kRehash) h = load_hash(keys, i, g.seed, hashed);
+          uint64_t fp, i1, i2;
+          place<POL>(h, g, fp, i1, i2);
+          st = rng_init(g.seed, h, g.worker) + kGolden;
+          cur_b = i1;
+          cur_tag = fp;
+          if (smix(st) & 1u) {
+            cur_b = i2;
+            cur_tag = make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g);
+          }
+          n = 1;
+          have = true;
+        }
+      }
+      if (base + __popc(need) >= total) drained = true;  // the cursor only grows
+    }
+    if (!__any_sync(0xffffffffu, have)) break;
+    if (!have) continue;
+    // ---- one BFS round ----
+    bool done = false;
+    st += kGolden;
+    const uint32_t start = (uint32_t)(smix(st) % kB);
+    uint64_t* base_w = words + cur_b * WPB;
+    uint64_t cw[WPB];
+    ld_bucket_rw<WPB>(base_w, cw);
+    uint64_t occm = 0;
+#pragma unroll
+    for (int q = 0; q < WPB; ++q) {
+      const uint64_t z = L::zeros(cw[q]);
+#pragma unroll
+      for (int s = 0; s < kTpw; ++s)
+        if (!((z >> (s * F + F - 1)) & 1u)) occm |= 1ull << (q * kTpw + s);
+    }
+    const uint64_t rot = start ? (((occm >> start) | (occm << (kB - start))) & kAll) : occm;
+    const uint32_t pc = (uint32_t)__popcll(rot);
+    const uint32_t cnt = pc < kLim ? pc : kLim;
+    if (cnt == 0) {  // drained by concurrent deletes: take a direct slot
+      const uint32_t e = empty_lanes<F, WPB>(cw);
+      if (try_insert_snap<F, WPB>(words, cur_b, cur_tag, cw) >= 0) {
+        rm_filled(rm, cur_b, e);
+        done = true;
+      }
+    } else {
+      uint32_t word[kLim], bit[kLim];
+      uint64_t rr = rot;
+#pragma unroll
+      for (uint32_t c = 0; c < kLim; ++c) {
+        word[c] = bit[c] = 0;
+        if (c >= cnt) continue;
+        uint32_t sl = (uint32_t)(__ffsll((long long)rr) - 1) + start;
+        sl = sl >= kB ? sl - kB : sl;
+        rr &= rr - 1;
+        const uint64_t ct = L::get(snap_word<WPB>(cw, sl / kTpw), sl % kTpw);
+        uint64_t tc;
+        const uint64_t ab = alt_index<POL>(cur_b, tag_fp(ct, g), tag_choice(ct, g), g, tc);
+        word[c] = __ldcg(rm.bits + (ab >> 5));
+        bit[c] = (uint32_t)(ab & 31);
+      }
+      uint32_t roomm = 0;
+#pragma unroll
+      for (uint32_t c = 0; c < kLim; ++c) roomm |= ((word[c] >> bit[c]) & 1u) << c;
+      const uint32_t chosen = roomm ? (uint32_t)(__ffs((int)roomm) - 1) : cnt - 1;
+      const uint32_t os = nth_candidate<kB>(rot, chosen, start);
+      const uint64_t ow = snap_word<WPB>(cw, os / kTpw);
+      const uint64_t otag = L::get(ow, os % kTpw);
+      uint64_t tc;
+      const uint64_t cfp = tag_fp(otag, g);
+      const uint64_t alt_b = alt_index<POL>(cur_b, cfp, tag_choice(otag, g), g, tc);
+      const uint64_t alt_tag = make_tag(cfp, tc, g);
+      if (roomm) {
+        // two-step relocation: copy the candidate out, then swap ourselves in
+        uint64_t aw[WPB];
+        ld_bucket_rw<WPB>(words + alt_b * WPB, aw);
+        const uint32_t e = empty_lanes<F, WPB>(aw);
+        const int aslot = try_insert_snap<F, WPB>(words, alt_b, alt_tag, aw);
+        if (aslot < 0) {
+          rm_filled(rm, alt_b, 0);  // the free lane raced away (a stale map bit)
+        } else {
+          rm_filled(rm, alt_b, e);
+          fault_origin_writer<F>(base_w + os / kTpw, os % kTpw, otag);
+          if (lane_cas_from<F>(base_w + os / kTpw, os % kTpw, otag, cur_tag, ow)) {
+            done = true;
+          } else {
+            lane_cas<F>(words + alt_b * WPB + aslot / kTpw, aslot % kTpw, alt_tag, 0);  // rollback
+            rm_freed(rm, alt_b);
+          }
+        }
+      } else if (lane_cas_from<F>(base_w + os / kTpw, os % kTpw, otag, cur_tag, ow)) {
+        // nobody has room: evict the last candidate and deepen (K:427-434)
+        cur_b = alt_b;
+        cur_tag = alt_tag;
+      }
+    }
+    const bool failed = !done && n >= g.max_evictions;
+    if (done || failed) {
+      const uint64_t lf = failed ? tag_fp(cur_tag, g) : 0;
+      rec[r] = ckf_record{i + ibase, lf, failed ? g.max_evictions : n, done ? 1u : 0u};
+      n_ok += done;
+      if (failed) ok[i] = 0;
+      if (ev) ev[i] = failed ? g.max_evictions : n;
+      if (lost) lost[i] = lf;
+      have = false;
+    } else {
+      ++n;
+    }
+  }
+  if (threadIdx.x == 0 && blockIdx.x == 0) ctr->n_records = total;
+  block_count_add(n_ok, 0, ctr, occ, +1);
+}
+
 // Delete (K:461-484): full-lane match, i1 with fp, then i2 with fp|choice.
 template <int F, int WPB, int POL>
 __global__ void __launch_bounds__(kBlock) delete_kernel(Geo g, uint64_t* __restrict__ words,
@@ -442,8 +591,20 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   }
   if (lrb < 1) lrb = 1;
   // coarse regions: at most kRMaxCoarse of them, each split into F2 <= kMaxF2 fine ones
-  uint32_t lrbc = lm > 9 ? lm - 9 : 0;
+  // log2 coarse regions: 2^8 (measured at 2^24 buckets: 2^9 -> 2^8 -> 2^7 coarse
+  // bins = 23.5 -> 22.8 -> 22.8 ms/step: longer bin-pass runs, split F2 16),
+  // or up to 2^9 when that saves a run (one offset bit less leaves one more
+  // index bit in the record)
+  const uint64_t per_rec = op == CKF_OP_QUERY ? 2 : 1;
+  auto runs_for = [&](uint32_t lrbc_) -> uint64_t {
+    uint64_t km = (1ull << (64 - (pb + lrbc_ + 1))) - 2;
+    if (km > (1ull << 31) / per_rec) km = (1ull << 31) / per_rec;
+    return (n + km - 1) / km;
+  };
+  const uint32_t lc0 = (uint32_t)env_u64("CKF_COARSE_LOG2", 8);
+  uint32_t lrbc = lm > lc0 ? lm - lc0 : 0;
   if (lrbc < lrb) lrbc = lrb;
+  if (lc0 < 9 && lrbc > lrb && runs_for(lrbc - 1) < runs_for(lrbc)) --lrbc;
   if (lrbc - lrb > ceil_log2(kMaxF2)) return pl;
   const uint64_t R1 = (m + (1ull << lrbc) - 1) >> lrbc;
   if (R1 > (uint64_t)kRMaxCoarse) return pl;
@@ -451,7 +612,6 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   if (ish > 62) return pl;
   // keys per run: the index field (all-ones is the filler), 32-bit miss-entry
   // indices, and < 2^32 record slots over the coarse bins (dual query records)
-  const uint64_t per_rec = op == CKF_OP_QUERY ? 2 : 1;
   uint64_t kmax = (1ull << (64 - ish)) - 2;
   if (kmax > (1ull << 31) / per_rec) kmax = (1ull << 31) / per_rec;
   const uint64_t kenv = env_u64("CKF_MAX_RUN_KEYS", 0);  // developer knob: exercise multi-run calls
@@ -498,7 +658,7 @@ static RLayout rlayout_for(const RPlan& pl, int op) {
   L.mode = L.n_miss + 4ull * kMaxProbeGrid;
   L.ctr_end = align256(L.mode + 8);
   L.qstart = L.ctr_end;  // insert: eviction-queue length before this run (not zeroed per run)
-  L.room = align256(L.qstart + 8);  // insert: room bit per bucket
+  L.room = align256(L.qstart + 16);  // insert: [qstart, eviction cursor], then the room bit per bucket
   L.bin1 = align256(L.room + (op == CKF_OP_INSERT ? ((uint64_t)pl.R << pl.lrb) / 8 : 0));
   L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
   L.miss = align256(L.binf + pl.R * pl.capf * 8);
@@ -570,19 +730,19 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
   int st;
   // phase 1: primary buckets
-  region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, 3), kBThreads, kBinSmem, s>>>(
+  region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, kBinBlocks), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, n, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   // phase 2: the misses, on their alternate buckets
   if (cudaMemsetAsync(ws, 0, L.bin_ctr_end, s) != cudaSuccess) return cuda_error();
-  region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * 3 + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
+  region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * kBinBlocks + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, 0, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * 3, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
@@ -662,10 +822,20 @@ struct InsertArgs {
 };
 
 template <int F, int WPB, int POL>
-static int launch_evict(const InsertArgs& a, uint64_t off, const unsigned long long* qstart, RoomMap rm) {
+static int launch_evict(const InsertArgs& a, uint64_t off, const unsigned long long* qstart, RoomMap rm,
+                        unsigned long long* cursor = nullptr) {
   // the queue length is only known on the device: a fixed full-residency grid
   // strides over it (empty queues exit immediately)
   const unsigned egrid = (unsigned)sm_count() * kEvictBlocks;
+  if constexpr (WPB > 0) {
+    if (rm.bits && cursor && a.g.eviction == CKF_EVICT_BFS && !getenv("CKF_EVICT_CHAINS")) {
+      if (cudaMemcpyAsync(cursor, qstart, 8, cudaMemcpyDeviceToDevice, a.s) != cudaSuccess) return cuda_error();
+      evict_bfs_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok + off, a.ev ? a.ev + off : nullptr,
+                                                               a.lost ? a.lost + off : nullptr, a.rec, a.cap, a.ctr,
+                                                               a.occ, a.keys + off, a.hashed, off, cursor, rm);
+      return status();
+    }
+  }
   evict_kernel<F, WPB, POL><<<egrid, kBlock, 0, a.s>>>(a.g, a.words, a.ok + off, a.ev ? a.ev + off : nullptr,
                                                        a.lost ? a.lost + off : nullptr, a.rec, a.cap, a.ctr, a.occ,
                                                        a.keys + off, a.hashed, off, qstart, rm);
@@ -699,7 +869,7 @@ struct InsertOp {
           if (st) return st;
           const RWork w = rwork_view(a.t.ws, a.t.RL, a.t.rpl);
           const RoomMap rm{getenv("CKF_NO_ROOM_MAP") ? nullptr : w.room};
-          if ((st = launch_evict<F, WPB, POL>(a, off, qstart, rm))) return st;
+          if ((st = launch_evict<F, WPB, POL>(a, off, qstart, rm, qstart + 1))) return st;
         }
         return CKF_OK;
       }

@@ -350,6 +350,7 @@ struct BinSmem {
   uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
   uint2 sg[kRMaxCoarse];               // {run start in rec, run start in the bin} (bulk: both even)
   uint32_t warp_sums[kBThreads / 32];
+  uint32_t total;                      // records placed in this tile (bulk: incl. run padding)
   uint32_t dst[kBTile];                // coalesced writer only (last: bulk-only kernels omit it)
 };
 constexpr uint32_t kBinSmemBulk = sizeof(BinSmem) - sizeof(uint32_t) * kBTile;
@@ -389,6 +390,7 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
   }
   __syncthreads();
   uint32_t run = sm.warp_sums[wid] + x - sum;
+  if (hi == nb) sm.total = run + sum;  // (every thread past the last bin writes the same value)
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const uint32_t r = lo + k;
@@ -477,8 +479,13 @@ __device__ __forceinline__ void bin_release() { bulk_wait_read(); }
 // blockIdx.y, one record for the alternate bucket.
 enum { SRC_KEYS = 0, SRC_MISS = 1 };
 
+#ifndef CKF_BIN_BLOCKS
+#define CKF_BIN_BLOCKS 3  // (measured: 4 per SM -- 64 registers, spills -- is slower)
+#endif
+constexpr int kBinBlocks = CKF_BIN_BLOCKS;  // resident bin CTAs per SM
+
 template <int OP, int F, int WPB, int POL, int SRC>
-__global__ void __launch_bounds__(kBThreads, 3)
+__global__ void __launch_bounds__(kBThreads, kBinBlocks)
     region_bin_kernel(Geo g, RPlan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n_keys, bool hashed,
                       RWork w, Sink sk, long long* occ) {
   extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
@@ -507,13 +514,18 @@ __global__ void __launch_bounds__(kBThreads, 3)
     uint64_t rec[kBItems];
     uint32_t pk[kBItems];  // bin << 16 | rank; 0xFFFFFFFF = no record
     if constexpr (SRC == SRC_KEYS) {
+      // item q of thread t: key t0 + (q / 2) * 2 * kBThreads + 2t + (q % 2) (pairs
+      // of 16 B, coalesced); dual: items [0, kBItems/2) are keys, the rest
+      // their i2 records.  The record's index field advances by a running
+      // 64-bit add (rec = idx << ish | ...).
+      const bool full = t0 + KT <= n;  // block-uniform: no bounds checks
       uint64_t kk[kBItems];
 #pragma unroll
       for (int q = 0; q < kBItems / 2; ++q) {
         const uint64_t i = t0 + (uint64_t)q * 2 * kBThreads + 2 * threadIdx.x;
         if (dual && q >= kBItems / 4) {
           kk[2 * q] = kk[2 * q + 1] = 0;
-        } else if (i + 1 < n && al16) {
+        } else if ((full || i + 1 < n) && al16) {
           asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                        : "=l"(kk[2 * q]), "=l"(kk[2 * q + 1])
                        : "l"(keys + i), "l"(pol));
@@ -523,25 +535,31 @@ __global__ void __launch_bounds__(kBThreads, 3)
         }
       }
       __syncthreads();
+      const uint64_t s1 = 1ull << pl.ish, s2 = (uint64_t)(2 * kBThreads) << pl.ish;
+      const uint64_t alt1 = 1ull << (pl.ish - 1);
+      const uint64_t pmask = (1ull << g.payload_bits) - 1u;
+      uint64_t ix = (t0 + 2 * threadIdx.x) << pl.ish;  // index field of item 0
 #pragma unroll
       for (int q = 0; q < kBItems; ++q) {
-        if (dual && q >= kBItems / 2) continue;  // filled with key q - kBItems/2's i2 record
-        const uint64_t i = t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
+        if (dual && q >= kBItems / 2) continue;  // filled with item q - kBItems/2's i2 record
+        const uint64_t ixq = (q & 1) ? ix + s1 : ix;
         const uint64_t h = hashed ? kk[q] : xxh64(kk[q], g.seed);
-        const bool mine = i < n && !(hashed && foreign(g, h));  // (padding of the sharded exchange: skipped)
-        const uint64_t fp0 = (h >> 32) & ((1ull << g.payload_bits) - 1u);
+        const bool in = full || t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1) < n;
+        const bool mine = in && !(hashed && foreign(g, h));  // (sharded padding: skipped)
+        const uint64_t fp0 = (h >> 32) & pmask;
         const uint64_t fp = fp0 ? fp0 : 1u;
-        const uint64_t i1 = reduce_index(h & 0xFFFFFFFFull, g);
-        const uint32_t b1 = (uint32_t)(i1 >> pl.lrbc);
-        rec[q] = rpack(i, 0u, i1 & lmask, fp, pl);
+        const uint64_t i1 = POL == CKF_POLICY_XOR ? (h & g.mask) : reduce_index(h & 0xFFFFFFFFull, g);
+        const uint32_t b1 = (uint32_t)i1 >> pl.lrbc;
+        rec[q] = ixq | ((uint64_t)((uint32_t)i1 & lmask) << pl.pb) | fp;
         pk[q] = mine ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
         if (q < kBItems / 2 && dual) {
           uint64_t cc;
           const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, cc);
-          const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
-          rec[q + kBItems / 2] = rpack(i, 1u, i2 & lmask, fp, pl);
+          const uint32_t b2 = (uint32_t)i2 >> pl.lrbc;
+          rec[q + kBItems / 2] = ixq | alt1 | ((uint64_t)((uint32_t)i2 & lmask) << pl.pb) | fp;
           pk[q + kBItems / 2] = mine ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
+        if (q & 1) ix += s2;
       }
     } else {
       __syncthreads();  // hist zeroed
@@ -575,7 +593,7 @@ __global__ void __launch_bounds__(kBThreads, 3)
       resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
     if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
-    else bin_write_coalesced(pl.R1, (uint32_t)(min(KT, n - t0) * (dual ? 2 : 1)), w.bin1, pl.cap1, sm, pol, ovf);
+    else bin_write_coalesced(pl.R1, sm.total, w.bin1, pl.cap1, sm, pol, ovf);
     __syncthreads();
   }
   bulk_wait_all();
@@ -586,8 +604,13 @@ __global__ void __launch_bounds__(kBThreads, 3)
 // split: coarse bin -> F2 fine bins (records re-based to the fine region)
 // ---------------------------------------------------------------------------
 
+#ifndef CKF_SPLIT_BLOCKS
+#define CKF_SPLIT_BLOCKS 4  // (measured: 3 -> 4 CTAs per SM, split 0.87 -> 0.79 ms at 2^28 slots)
+#endif
+constexpr int kSplitBlocks = CKF_SPLIT_BLOCKS;  // resident split CTAs per SM
+
 template <int OP, int F, int WPB, int POL>
-__global__ void __launch_bounds__(kBThreads, 3)
+__global__ void __launch_bounds__(kBThreads, kSplitBlocks)
     region_split_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
   extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
   BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
