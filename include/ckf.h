@@ -170,6 +170,18 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
                uint8_t* out, ckf_counters* counters, long long* occupancy, void* workspace,
                uint64_t workspace_bytes, unsigned flags, void* stream);
 
+/* Mixed batch (BASELINE configs[4]): key i runs ops[i] (CKF_OP_QUERY /
+ * CKF_OP_INSERT / CKF_OP_DELETE), all concurrently in one launch (+ the
+ * eviction pass for inserts whose pair is full).  Outside the reference's
+ * phase contract (filter.py:9-15): lookups use coherent loads, and a lookup is
+ * exact for keys whose membership the batch does not change.  out[i]: hit /
+ * stored / deleted.  records (record_cap) is the eviction queue as in
+ * ckf_insert; counters: n_ok = inserts stored, n_alt, n_queued; occupancy
+ * (nullable) += inserts - deletes. */
+int ckf_mixed(const ckf_params* p, uint64_t* words, const uint8_t* ops, const uint64_t* keys, uint64_t n,
+              uint8_t* out, ckf_record* records, uint64_t record_cap, ckf_counters* counters,
+              long long* occupancy, unsigned flags, void* stream);
+
 /* Multi-GPU routing (sharded.py steps 2-3): stable partition of key hashes
  * by owning shard (h >> shift) & (shards - 1), shards a power of two <= 8.
  * send[] receives the hashes grouped by shard in arrival order, order[p] the

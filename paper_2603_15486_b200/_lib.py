@@ -97,6 +97,7 @@ SIGNATURES = {
     "ckf_route_partition_padded": (ctypes.c_int, [_vp, _u64, _u32, _u32, _u64, _vp, _vp, _vp, _vp, _vp, _u64,
                                                   _vp]),
     "ckf_route_unpermute": (ctypes.c_int, [_vp, _vp, _u64, _u32, _vp, _vp]),
+    "ckf_mixed": (ctypes.c_int, [_P, _vp, _vp, _vp, _u64, _vp, _vp, _u64, _vp, _vp, ctypes.c_uint, _vp]),
     "ckf_route_workspace_bytes": (_u64, [_u64, _u32]),
     "ckf_route_partition": (ctypes.c_int, [_vp, _u64, _u32, _u32, _vp, _vp, _vp, _vp, _u64, _vp]),
     "ckf_kmer_workspace_bytes": (_u64, [_u64]),

@@ -409,6 +409,100 @@ __global__ void __launch_bounds__(kBlock) delete_kernel(Geo g, uint64_t* __restr
   block_count_add(n_ok, n_alt, ctr, occ, -1);
 }
 
+// Mixed batch (BASELINE configs[4]): one launch in which key i runs ops[i] --
+// CKF_OP_QUERY / CKF_OP_INSERT / CKF_OP_DELETE -- concurrently with the
+// others.  This steps outside the reference's phase contract (filter.py:9-15:
+// queries must not overlap mutations), so lookups read both buckets with
+// COHERENT loads (ld.relaxed.gpu, served by L2 where the CASes commit); a
+// lookup's answer is exact for keys whose membership the batch does not change
+// (SURVEY.md §7 hard part 6).  Inserts whose pair is full are queued for the
+// eviction pass like insert_kernel's; out[i] = hit / stored / deleted.
+template <int F, int WPB, int POL>
+__device__ __forceinline__ bool find_coherent(const uint64_t* words, uint64_t bucket, uint64_t fp, const Geo& g) {
+  using L = Lanes<F>;
+  const uint64_t keep = POL == CKF_POLICY_OFFSET ? ~L::kHigh : ~0ull;
+  const uint64_t pat = L::bcast(fp);
+  if constexpr (WPB > 0) {
+    uint64_t w[WPB];
+    ld_bucket_rw<WPB>(words + bucket * WPB, w);
+    uint64_t any = 0;
+#pragma unroll
+    for (int j = 0; j < WPB; ++j) any |= L::zeros((w[j] & keep) ^ pat);
+    return any != 0;
+  } else {
+    for (uint32_t j = 0; j < g.wpb; ++j)
+      if (L::zeros((ld_word_rw(words + bucket * g.wpb + j) & keep) ^ pat)) return true;
+    return false;
+  }
+}
+
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBlock) mixed_kernel(Geo g, uint64_t* __restrict__ words,
+                                                       const uint8_t* __restrict__ ops,
+                                                       const uint64_t* __restrict__ keys, uint64_t n,
+                                                       uint8_t* __restrict__ out, ckf_record* __restrict__ rec,
+                                                       uint64_t cap, ckf_counters* ctr, long long* occ, bool hashed) {
+  uint32_t n_ins = 0, n_del = 0, n_alt = 0;
+  const int lane_id = threadIdx.x & 31;
+  for (uint64_t t0 = blockIdx.x * (uint64_t)kBlock; t0 < n; t0 += (uint64_t)gridDim.x * kBlock) {
+    const uint64_t i = t0 + threadIdx.x;
+    bool need = false;
+    uint64_t h = 0, fp = 0, i1 = 0, i2 = 0;
+    if (i < n) {
+      const uint8_t op = ops[i];
+      h = load_hash(keys, i, g.seed, hashed);
+      place<POL>(h, g, fp, i1, i2);
+      const uint64_t tag2 = make_tag(fp, POL == CKF_POLICY_OFFSET ? 1u : 0u, g);
+      bool r = false;
+      if (hashed && foreign(g, h)) {
+        r = false;
+      } else if (op == CKF_OP_INSERT) {
+        r = try_insert_any<F, WPB>(words, i1, fp, g) >= 0;
+        if (!r) {
+          ++n_alt;
+          r = try_insert_any<F, WPB>(words, i2, tag2, g) >= 0;
+        }
+        n_ins += r;
+        need = !r;
+        r = true;  // a queued key stays stored unless the eviction pass fails it
+      } else if (op == CKF_OP_DELETE) {
+        r = remove_tag_any<F, WPB>(words, i1, fp, g) >= 0;
+        if (!r) {
+          ++n_alt;
+          r = remove_tag_any<F, WPB>(words, i2, POL == CKF_POLICY_OFFSET ? tag2 : fp, g) >= 0;
+        }
+        n_del += r;
+      } else {
+        r = find_coherent<F, WPB, POL>(words, i1, fp, g);
+        if (!r) {
+          ++n_alt;
+          r = find_coherent<F, WPB, POL>(words, i2, fp, g);
+        }
+      }
+      out[i] = r;
+    }
+    const unsigned qmask = __ballot_sync(0xffffffffu, need);
+    if (qmask) {
+      unsigned long long qbase = 0;
+      const int leader = __ffs(qmask) - 1;
+      if (lane_id == leader) qbase = atomicAdd(&ctr->n_queued, (unsigned long long)__popc(qmask));
+      qbase = __shfl_sync(0xffffffffu, qbase, leader);
+      if (need) {
+        const uint64_t pos = qbase + __popc(qmask & ((1u << lane_id) - 1u));
+        if (pos < cap) {
+          rec[pos] = ckf_record{i, h, 0u, 0u};
+        } else {  // queue overflow: evict in place
+          const Outcome o = evict_any<F, WPB, POL>(words, h, fp, i1, i2, g);
+          n_ins += o.ok;
+          out[i] = (uint8_t)o.ok;
+        }
+      }
+    }
+  }
+  block_count_add(n_ins, n_alt, ctr, occ, +1);
+  block_count_add(n_del, 0, nullptr, occ, -1);
+}
+
 // Parity mode: the reference's sequential insert_batch (K:510-529), one
 // device thread, same key order, same PRNG stream; bit-identical table.
 template <int F, int WPB, int POL>
@@ -923,6 +1017,35 @@ struct DeleteOp {
   }
 };
 
+struct MixedArgs {
+  Geo g;
+  uint64_t* words;
+  const uint8_t* ops;
+  const uint64_t* keys;
+  uint64_t n;
+  uint8_t* out;
+  ckf_record* rec;
+  uint64_t cap;
+  ckf_counters* ctr;
+  long long* occ;
+  bool hashed;
+  cudaStream_t s;
+};
+
+template <int F, int WPB, int POL>
+struct MixedOp {
+  static int run(const MixedArgs& a) {
+    mixed_kernel<F, WPB, POL><<<grid_for(a.n, kBlock, 16), kBlock, 0, a.s>>>(a.g, a.words, a.ops, a.keys, a.n, a.out,
+                                                                         a.rec, a.cap, a.ctr, a.occ, a.hashed);
+    int st = status();
+    if (st || !a.cap) return st;
+    evict_kernel<F, WPB, POL><<<(unsigned)sm_count() * kEvictBlocks, kBlock, 0, a.s>>>(
+        a.g, a.words, a.out, nullptr, nullptr, a.rec, a.cap, a.ctr, a.occ, a.keys, a.hashed, 0, nullptr,
+        RoomMap{nullptr});
+    return status();
+  }
+};
+
 template <int F, int WPB, int POL>
 struct PlaceOp {
   static int run(Geo g, const uint64_t* keys, uint64_t n, uint64_t* fp, uint64_t* i1, uint64_t* i2, bool hashed,
@@ -1391,6 +1514,19 @@ int ckf_delete(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   DeleteArgs a{geo_from(*p), words, keys, n, out, counters, occupancy, (flags & CKF_INPUT_HASHED) != 0,
                (flags & CKF_MODE_SEQUENTIAL) != 0, s, choose(p, n, CKF_OP_DELETE, flags, keys, workspace, workspace_bytes)};
   return dispatch3<DeleteOp>(p, words, a);
+}
+
+int ckf_mixed(const ckf_params* p, uint64_t* words, const uint8_t* ops, const uint64_t* keys, uint64_t n,
+              uint8_t* out, ckf_record* records, uint64_t record_cap, ckf_counters* counters, long long* occupancy,
+              unsigned flags, void* stream) {
+  if (!params_ok(p) || !words || !counters) return CKF_EINVAL;
+  cudaStream_t s = (cudaStream_t)stream;
+  if (cudaMemsetAsync(counters, 0, sizeof(ckf_counters), s) != cudaSuccess) return cuda_error();
+  if (n == 0) return CKF_OK;
+  if (!ops || !keys || !out || (record_cap && !records)) return CKF_EINVAL;
+  MixedArgs a{geo_from(*p), words, ops, keys, n, out, records, records ? record_cap : 0, counters, occupancy,
+              (flags & CKF_INPUT_HASHED) != 0, s};
+  return dispatch3<MixedOp>(p, words, a);
 }
 
 uint64_t ckf_route_workspace_bytes(uint64_t n, uint32_t shards) {

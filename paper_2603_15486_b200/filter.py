@@ -460,6 +460,39 @@ class CuckooFilter:
             if self._debug:
                 self._exit_mutate()
 
+    def mixed_batch(self, ops, keys, *, hashed: bool = False):
+        """Mixed lookup / insert / delete batch (BASELINE configs[4]) in ONE launch.
+
+        ``ops[i]`` in {0: lookup, 1: insert, 2: delete} (``OP_QUERY`` /
+        ``OP_INSERT`` / ``OP_DELETE``).  Returns per key: hit / stored /
+        deleted.  An extension past the reference's phase contract
+        (filter.py:9-15): all ops run concurrently, lookups with coherent
+        loads, so a lookup's answer is exact for keys whose membership the
+        batch does not change."""
+        if self._debug:
+            self._enter_mutate()
+        try:
+            k, kind = self._as_keys(keys)
+            if isinstance(ops, torch.Tensor):
+                o = ops.to(self.device, torch.uint8).contiguous()
+            else:
+                o = torch.from_numpy(np.ascontiguousarray(ops, dtype=np.uint8)).to(self.device)
+            n = k.numel()
+            if o.numel() != n:
+                raise ValueError("ops and keys differ in length")
+            with torch.cuda.device(self.device):
+                out = torch.empty(n, dtype=torch.uint8, device=self.device)
+                rec = torch.empty(max(n, 1) * _lib.RECORD_BYTES, dtype=torch.uint8, device=self.device)
+                _lib.check(_lib.lib().ckf_mixed(
+                    ctypes.byref(self._params), self.words_device.data_ptr(), o.data_ptr(), k.data_ptr(), n,
+                    out.data_ptr(), rec.data_ptr(), n, self._ctr.data_ptr(), self._occ.data_ptr(),
+                    _lib.INPUT_HASHED if hashed else 0, self._stream()))
+            self.last_schedule = ("direct", 0)
+            return self._answer(out.view(torch.bool), kind)
+        finally:
+            if self._debug:
+                self._exit_mutate()
+
     # ---- one C-ABI launch on device buffers (current stream) ----
 
     def _launch(self, op: int, k: torch.Tensor, out: torch.Tensor, flags: int, p=None,

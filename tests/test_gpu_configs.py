@@ -219,3 +219,46 @@ def test_mixed_stream_fpr(f):
         assert abs(k / len(neg) - model) / model < 0.3
     else:
         assert k <= 5  # eps ~ 4e-9
+
+
+@pytest.mark.parametrize("f", [8, 16, 32])
+@pytest.mark.parametrize("tiled", [False, True], ids=["direct-prefill", "region-prefill"])
+def test_mixed_batch_one_launch(f, tiled):
+    """configs[4] as ONE concurrent launch per round (CuckooFilter.mixed_batch):
+    25 % inserts of new keys, 25 % deletes of keys from earlier rounds, 50 %
+    lookups of keys whose membership the round does not change -- interleaved
+    in one shuffled batch.  Every lookup hits, every insert and delete
+    succeeds, occupancy tracks the live set, deleting the live set afterwards
+    empties the table, and the FPR on disjoint negatives sits inside the
+    99.9 % interval of the oracle's on the same live set."""
+    cfg = FilterConfig(bucket_count=1 << 14, fingerprint_bits=f, bucket_slots=16, eviction="bfs", seed=f)
+    slots = cfg.total_slots
+    rng = np.random.default_rng(300 + f)
+    pool = rng.integers(0, 1 << 62, size=4 * slots, dtype=np.uint64)
+    filt = CuckooFilter(cfg, tiled=tiled)
+    live = pool[: slots // 2].copy()
+    assert filt.insert_batch(live).n_failed == 0
+    nxt, batch = slots // 2, 8192
+    for _ in range(25):
+        new = pool[nxt: nxt + batch // 4]
+        nxt += batch // 4
+        pick = rng.choice(len(live), size=batch // 4, replace=False)
+        doomed = live[pick]
+        survivors = np.delete(live, pick)
+        probe = survivors[rng.integers(0, len(survivors), size=batch // 2)]
+        keys = np.concatenate([new, doomed, probe])
+        ops = np.concatenate([np.full(len(new), 1), np.full(len(doomed), 2), np.full(len(probe), 0)]).astype(np.uint8)
+        perm = rng.permutation(len(keys))
+        res = filt.mixed_batch(ops[perm], keys[perm])
+        assert res.all(), "a lookup of a fixed key missed, or an insert / delete failed"
+        live = np.concatenate([survivors, new])
+        assert len(filt) == len(live)
+    neg = rng.integers(1 << 62, 1 << 63, size=2_000_000, dtype=np.uint64)
+    k = int(filt.query_batch(neg).sum())
+    ref = oracle.OracleFilter(oracle.cfg_from(cfg))
+    ref.insert_batch(live)
+    k_ref = int(ref.query_batch(neg, threads=8).sum())
+    lo, hi = cp(k, len(neg))
+    lo_r, hi_r = cp(k_ref, len(neg))
+    assert lo <= hi_r and lo_r <= hi, (k, k_ref)
+    assert filt.delete_batch(live).all() and len(filt) == 0 and not filt.words.any()
