@@ -26,13 +26,13 @@ for d in ours:
     d["op"] = (int(args[0]) if args and m.group(1).startswith(("tile", "region"))
                and m.group(1) != "region_sample_kernel" else None)
     # a new op call starts at its first pass: the keys' bin kernel (region SRC_KEYS = 0) or a direct kernel
-    d["start"] = (d["short"] in ("tile_bin_kernel", "region_sample_kernel")
+    d["start"] = (d["short"] in ("region_sample_kernel",)
                   or (d["short"] == "region_bin_kernel" and args[-1] == "0")
                   or d["short"] in ("insert_kernel", "query_kernel", "delete_kernel"))
 
 
 def op_of(d):
-    if d["short"] in ("insert_kernel", "evict_kernel"):
+    if d["short"] in ("insert_kernel", "evict_kernel", "evict_bfs_kernel"):
         return "insert"
     if d["short"] in ("query_kernel", "region_sample_kernel"):
         return "query"
