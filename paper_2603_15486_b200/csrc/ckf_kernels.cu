@@ -202,7 +202,10 @@ __global__ void __launch_bounds__(kBlock) insert_kernel(Geo g, uint64_t* __restr
 }
 
 // Eviction pass over the queued keys (the ~4% whose pair was full at 95% load).
-constexpr int kEvictBlocks = 3;  // resident blocks per SM (<= 85 registers: the BFS chain's snapshots)
+#ifndef CKF_EVICT_BLOCKS
+#define CKF_EVICT_BLOCKS 3
+#endif
+constexpr int kEvictBlocks = CKF_EVICT_BLOCKS;  // resident blocks per SM (<= 85 registers: the BFS chain's snapshots)
 // Queue entries [*qstart, n_queued) belong to this run (a chunk of the call
 // whose keys start at batch index ibase; keys / ok / ev / lost are the run's).
 template <int F, int WPB, int POL>
@@ -819,7 +822,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   constexpr uint32_t kBinSmem = sizeof(BinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
-  allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmemBulk);
+  allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmem);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmem);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
   int st;
@@ -827,7 +830,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, kBinBlocks), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, n, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
@@ -836,7 +839,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * kBinBlocks + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, 0, hashed, w, sk, mocc);
   if ((st = status())) return st;
-  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmemBulk, s>>>(g, pl, words, w, sk, mocc);
+  region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;

@@ -350,10 +350,7 @@ struct BinSmem {
   uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
   uint2 sg[kRMaxCoarse];               // {run start in rec, run start in the bin} (bulk: both even)
   uint32_t warp_sums[kBThreads / 32];
-  uint32_t total;                      // records placed in this tile (bulk: incl. run padding)
-  uint32_t dst[kBTile];                // coalesced writer only (last: bulk-only kernels omit it)
 };
-constexpr uint32_t kBinSmemBulk = sizeof(BinSmem) - sizeof(uint32_t) * kBTile;
 
 // sm.cnt (records per bin) -> sm.sg.x (exclusive scan of the padded run
 // lengths) and sm.sg.y (one global reservation per non-empty bin)
@@ -390,7 +387,6 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
   }
   __syncthreads();
   uint32_t run = sm.warp_sums[wid] + x - sum;
-  if (hi == nb) sm.total = run + sum;  // (every thread past the last bin writes the same value)
 #pragma unroll
   for (int k = 0; k < 2; ++k) {
     const uint32_t r = lo + k;
@@ -402,40 +398,8 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
   }
 }
 
-template <bool kBulk>
-__device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc, uint64_t cap) {
-  const uint2 sg = sm.sg[b];
-  const uint32_t p = sg.x + rank;
-  sm.rec[p] = rc;
-  if (!kBulk) {  // slot in the bin array (bin * cap + offset < 2^32), or none: bin full
-    const uint32_t o = sg.y + rank;
-    sm.dst[p] = o < cap ? b * (uint32_t)cap + o : 0xFFFFFFFFu;
-  }
-}
-
-// Coalesced writer (short runs): thread p stores sorted record p.  Caller: all
-// threads, after bin_place<false>; records of full bins go to ovf(rec, bin).
-template <class Ovf>
-__device__ __forceinline__ void bin_write_coalesced(uint32_t nb, uint32_t total, uint64_t* __restrict__ out,
-                                                    uint64_t cap, BinSmem& sm, uint64_t pol, Ovf&& ovf) {
-  __syncthreads();
-  for (uint32_t p = threadIdx.x; p < total; p += kBThreads) {
-    const uint32_t d = sm.dst[p];
-    const uint64_t rc = sm.rec[p];
-    if (d != 0xFFFFFFFFu) {
-      st_stream_ef(out + d, rc, pol);
-    } else {
-      // the bin of sorted position p: the last bin starting at or before p
-      // (empty bins share the start of the next one)
-      uint32_t lo = 0, hi = nb - 1;
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi + 1) >> 1;
-        if (sm.sg[mid].x <= p) lo = mid;
-        else hi = mid - 1;
-      }
-      ovf(rc, lo);
-    }
-  }
+__device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc) {
+  sm.rec[sm.sg[b].x + rank] = rc;
 }
 
 // Sends every (tile, bin) run to its bin with one bulk copy.  A run that does
@@ -582,18 +546,18 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
       }
     }
     __syncthreads();
-    constexpr bool kBulk = SRC == SRC_MISS;  // (measured: keys bin faster with coalesced stores)
-    bin_reserve<kBulk>(pl.R1, w.cnt1, sm);
+    // runs leave as bulk copies (measured at 16-record runs: 1.46 vs 1.49 ms
+    // for per-record coalesced stores, which also need a slot array)
+    bin_reserve<true>(pl.R1, w.cnt1, sm);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
-      if (pk[q] != 0xFFFFFFFFu) bin_place<kBulk>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q], pl.cap1);
+      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q]);
     auto ovf = [&](uint64_t rc, uint32_t b) {
       const uint64_t bucket = ((uint64_t)b << pl.lrbc) + ((rc >> pl.pb) & lmask);
       resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
-    if constexpr (kBulk) bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
-    else bin_write_coalesced(pl.R1, sm.total, w.bin1, pl.cap1, sm, pol, ovf);
+    bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
     __syncthreads();
   }
   bulk_wait_all();
@@ -657,7 +621,7 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
-      if (pk[q] != 0xFFFFFFFFu) bin_place<true>(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep, pl.capf);
+      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep);
     bin_write(pl.F2, w.binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](uint64_t rc, uint32_t f) {
       const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
       resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
