@@ -673,7 +673,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   RPlan pl{};
   ok = false;
   const uint32_t wpb = p->words_per_bucket;
-  if (wpb != 2 && wpb != 4 && wpb != 8) return pl;
+  if (wpb != 1 && wpb != 2 && wpb != 4 && wpb != 8) return pl;
   const uint64_t m = p->bucket_count;
   const uint32_t pb = p->payload_bits;
   if (pb > 24 || m < 2 || m > (1ull << 32) || n == 0) return pl;
@@ -880,7 +880,7 @@ struct QueryArgs {
 template <int F, int WPB, int POL>
 struct QueryOp {
   static int run(const QueryArgs& a) {
-    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region) {
         for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
           uint64_t off, cnt;
@@ -947,7 +947,7 @@ struct InsertOp {
                                                    a.occ, a.hashed);
       return status();
     }
-    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region && a.cap) {
         // every key counts as stored until the eviction pass says otherwise
         if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
@@ -1001,7 +1001,7 @@ struct DeleteOp {
       seq_delete_kernel<F, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.occ, a.hashed);
       return status();
     }
-    if constexpr ((WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
       if (a.t.region) {
         for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
           uint64_t off, cnt;
@@ -1461,7 +1461,7 @@ uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned f
   if (!params_ok(p) || !region_wanted(p, n, flags)) return 0;
   if (op == CKF_OP_INSERT || op == CKF_OP_DELETE || op == CKF_OP_QUERY) {
     const uint32_t f = p->fingerprint_bits, wpb = p->words_per_bucket;
-    if (f == 32 || (wpb != 2 && wpb != 4 && wpb != 8)) return 0;
+    if (f == 32 || (wpb != 1 && wpb != 2 && wpb != 4 && wpb != 8)) return 0;
   }
   bool ok;
   const RPlan rp = make_rplan(p, n, op, flags, ok);

@@ -762,10 +762,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
         while (r < pl.R && region_count(r) == 0) r += gridDim.x;
       return r;
     };
+    // Bulk copies move 16 B granules: a region of an odd number of 8-byte
+    // buckets (WPB = 1, the last region of an odd-m offset table) moves its
+    // last word with a plain load / store.
     auto load_table = [&](uint32_t r) {  // consumer thread 0
-      const uint32_t nb = region_buckets(r);
-      mbar_expect_tx(tbar, nb * bbytes);
-      bulk_g2s(tab, words + ((uint64_t)r << pl.lrb) * WPB, nb * bbytes, tbar);
+      const uint32_t nbytes = region_buckets(r) * bbytes, bulk = nbytes & ~15u;
+      const uint64_t* src = words + ((uint64_t)r << pl.lrb) * WPB;
+      if (bulk != nbytes) tab[bulk / 8] = src[bulk / 8];  // (before the arrive that releases the slice)
+      mbar_expect_tx(tbar, bulk);
+      if (bulk) bulk_g2s(tab, src, bulk, tbar);
       const uint32_t rn = next_region(r + gridDim.x);
       if (rn < pl.R) prefetch_l2(words + ((uint64_t)rn << pl.lrb) * WPB, region_buckets(rn) * bbytes);
     };
@@ -899,7 +904,9 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint32_t rn = next_region(r + gridDim.x);
       if (tid == 0) {
         if (kMut && cn) {
-          bulk_s2g(words + b0 * WPB, tab, region_buckets(r) * bbytes);
+          const uint32_t nbytes = region_buckets(r) * bbytes, bulk = nbytes & ~15u;
+          if (bulk != nbytes) words[b0 * WPB + bulk / 8] = tab[bulk / 8];
+          if (bulk) bulk_s2g(words + b0 * WPB, tab, bulk);
           bulk_wait_read();  // the slice has left shared memory
         }
         if (rn < pl.R) load_table(rn);

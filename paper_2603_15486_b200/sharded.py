@@ -308,15 +308,16 @@ class ShardedCuckooFilter:
         """Keys past their block's capacity (adversarial skew): if any rank
         spilled, every rank runs an exact-split round over its unanswered keys."""
         if route is None or route.kind != "padded":
-            return
+            return None
         route.routed.synchronize()  # the routing kernels only (the exchange is in flight)
         if sum(self._host_allgather(int(route.spill_host.item()))) == 0:
-            return
+            return None
         idx = torch.nonzero(out == 0xFF).flatten()
         recv, r2 = self._scatter_exact(self._hash(route.keys[idx]))
         res = getattr(self.local, op)(recv, hashed=True)
-        res = res.ok if op == "insert_batch" else res
-        out[idx] = self._back(torch.as_tensor(res).to(self.device).to(torch.uint8), r2)
+        ans = torch.as_tensor(res.ok if op == "insert_batch" else res).to(self.device)
+        out[idx] = self._back(ans.to(torch.uint8), r2)
+        return ans
 
     # ---- batch API ----
 
@@ -326,12 +327,15 @@ class ShardedCuckooFilter:
         local_ok = res.ok if op == "insert_batch" else res
         local_ok = torch.as_tensor(local_ok).to(self.device)
         out = self._back(local_ok.to(torch.uint8), route, fill=0xFF)
-        self._spill_round(route, out, op)
-        return out.view(torch.bool) if out.dtype == torch.uint8 else out, res, route, local_ok
+        spill = self._spill_round(route, out, op)
+        return out.view(torch.bool) if out.dtype == torch.uint8 else out, res, route, local_ok, spill
 
     def insert_batch(self, keys, workers: int = 1) -> ShardedInsertResult:
-        ok, res, route, local_ok = self._run(keys, "insert_batch")
-        n_ok = local_ok.to(torch.int64).sum().reshape(1)
+        ok, res, route, local_ok, spill = self._run(keys, "insert_batch")
+        ctr = getattr(res, "_ctr", None)  # the local kernels' counters: real inserts only, no padding
+        n_ok = ctr[0:1].clone() if ctr is not None else local_ok.to(torch.int64).sum().reshape(1)
+        if spill is not None:
+            n_ok += spill.to(torch.int64).sum()
         if self.world > 1:
             dist.all_reduce(n_ok, group=self.group)
 
