@@ -579,7 +579,18 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
   extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
   BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
   const uint64_t pol = evict_first_policy();
-  const uint32_t tiles_per_bin = (uint32_t)((pl.cap1 + kBTile - 1) / kBTile);
+  // tiles per coarse bin from the fullest bin of THIS pass (phase 2 bins hold
+  // ~10 % of phase 1's records: no walk over the empty tail of every bin)
+  __shared__ uint32_t s_max;
+  if (threadIdx.x == 0) s_max = 0;
+  __syncthreads();
+  uint32_t mx = 0;
+  for (uint32_t c = threadIdx.x; c < pl.R1; c += kBThreads) mx = max(mx, w.cnt1[(size_t)c * kCntStride]);
+  mx = __reduce_max_sync(0xffffffffu, mx);
+  if ((threadIdx.x & 31) == 0) atomicMax(&s_max, mx);
+  __syncthreads();
+  const uint64_t maxcnt = s_max < pl.cap1 ? s_max : pl.cap1;
+  const uint32_t tiles_per_bin = (uint32_t)((maxcnt + kBTile - 1) / kBTile);
   const uint64_t tiles = (uint64_t)pl.R1 * tiles_per_bin;
   const uint32_t fshift = pl.pb + pl.lrb;  // offset bits above the fine offset
   const uint32_t fmask = pl.F2 - 1u;
