@@ -257,10 +257,18 @@ def run_ours(args) -> None:
     world = int(os.environ.get("WORLD_SIZE", 1))
     rank = int(os.environ.get("RANK", 0))
     local = int(os.environ.get("LOCAL_RANK", 0))
+    # BENCH_BACKEND=gloo (developer check of the multi-rank path on a box with
+    # fewer GPUs than ranks: ranks share the devices, gloo moves the data)
+    backend = os.environ.get("BENCH_BACKEND", "nccl")
+    if backend != "nccl":
+        local %= torch.cuda.device_count()
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
 
     from paper_2603_15486_b200 import CuckooFilter, FilterConfig, _lib
     from paper_2603_15486_b200.sharded import ShardedCuckooFilter

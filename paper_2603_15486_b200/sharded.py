@@ -80,10 +80,11 @@ class ShardedInsertResult:
     ``evictions`` / ``lost_fingerprints`` (filter.py:95-112) are routed back
     on first access -- a collective: every rank must read them together."""
 
-    def __init__(self, ok: torch.Tensor, n_ok_global: torch.Tensor, n: int, back=None):
+    def __init__(self, ok: torch.Tensor, n_ok_global: torch.Tensor, n: int, back=None, n_alt=None):
         self.ok = ok
         self._n_ok = n_ok_global
         self._n = n
+        self._n_alt = n_alt  # () -> global count of keys that probed their alternate bucket
         self._back = back  # () -> (evictions, lost) in caller order, or None
         self._ev = self._lost = None
 
@@ -109,6 +110,11 @@ class ShardedInsertResult:
     @property
     def n_ok_global(self) -> int:
         return int(self._n_ok.item())
+
+    @property
+    def n_alt(self) -> int:
+        """Keys (all ranks) whose primary bucket was full; a collective."""
+        return self._n_alt() if self._n_alt is not None else 0
 
     @property
     def n_ok(self) -> int:
@@ -344,7 +350,13 @@ class ShardedCuckooFilter:
             lost = torch.as_tensor(res.lost_fingerprints).to(self.device).view(torch.int64)
             return self._back(ev, route), self._back(lost, route)
 
-        return ShardedInsertResult(ok, n_ok, ok.numel(), back if hasattr(res, "evictions") else None)
+        def n_alt():
+            t = (ctr[3:4].clone() if ctr is not None else torch.zeros(1, dtype=torch.int64, device=self.device))
+            if self.world > 1:
+                dist.all_reduce(t, group=self.group)
+            return int(t.item())
+
+        return ShardedInsertResult(ok, n_ok, ok.numel(), back if hasattr(res, "evictions") else None, n_alt)
 
     def query_batch(self, keys, workers: int = 1) -> torch.Tensor:
         return self._run(keys, "query_batch")[0]
