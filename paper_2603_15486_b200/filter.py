@@ -43,6 +43,8 @@ _VERSION = 1
 # magic, version, f, b, m, policy, occupancy, seed (filter.py:38-42)
 _HEADER = struct.Struct("<4sIIIQIQQ")
 
+_OP_NAMES = {_lib.OP_QUERY: "query", _lib.OP_INSERT: "insert", _lib.OP_DELETE: "delete"}
+
 _REC_DTYPE = np.dtype([("index", "<u8"), ("lost", "<u8"), ("evictions", "<u4"), ("ok", "<u4")])
 assert _REC_DTYPE.itemsize == _lib.RECORD_BYTES
 
@@ -242,7 +244,7 @@ class CuckooFilter:
             self.words_device = torch.zeros(cfg.total_words, dtype=torch.int64, device=self.device)
             # [0] occupancy (kernels add/subtract), [1..4] scratch counters for scalar ops
             self._occ = torch.zeros(1, dtype=torch.int64, device=self.device)
-            self._ctr = torch.zeros(4, dtype=torch.int64, device=self.device)
+            self._ctrs = {}  # per-CUDA-stream device counters of query / delete / mixed batches
         self._debug = debug_phase
         self._mut_depth = 0
         self._read_depth = 0
@@ -272,8 +274,27 @@ class CuckooFilter:
 
     @property
     def words(self) -> np.ndarray:
-        """Host snapshot of the word table as uint64 (the reference attribute)."""
+        """Host snapshot of the word table as uint64 (the reference attribute).
+
+        A copy: mutate the table through ``filt.words = array`` (written back
+        to HBM whole) or ``words_device``."""
         return self.words_device.cpu().numpy().view(np.uint64)
+
+    @words.setter
+    def words(self, value) -> None:
+        arr = np.ascontiguousarray(value, dtype=np.uint64).reshape(-1)
+        if arr.size != self.words_device.numel():
+            raise ValueError(f"word array has {arr.size} words, expected {self.words_device.numel()}")
+        self.words_device.copy_(torch.from_numpy(arr.view(np.int64)))
+
+    @property
+    def _ctr(self) -> torch.Tensor:
+        """This CUDA stream's counters (batches on other streams never share them)."""
+        s = self._stream()
+        c = self._ctrs.get(s)
+        if c is None:
+            c = self._ctrs[s] = torch.zeros(4, dtype=torch.int64, device=self.device)
+        return c
 
     def clear(self) -> None:
         self.words_device.zero_()
@@ -502,6 +523,12 @@ class CuckooFilter:
         L = _lib.lib()
         ws, wsb = self._workspace(p, n, op, flags)
         self.last_schedule = self._schedule_of(p, n, op, flags, k.data_ptr(), ws, wsb)
+        # an NVTX range per batch call (nsys / ncu --nvtx), named op[n]/schedule
+        with torch.cuda.nvtx.range(f"ckf.{_OP_NAMES[op]}[{n}]/{self.last_schedule[0]}"):
+            self._call(op, p, k, n, out, flags, rec, ctr, ws, wsb)
+
+    def _call(self, op, p, k, n, out, flags, rec, ctr, ws, wsb) -> None:
+        L = _lib.lib()
         if op == _lib.OP_INSERT:
             _lib.check(L.ckf_insert(
                 ctypes.byref(p), self.words_device.data_ptr(), k.data_ptr(), n, out.data_ptr(),
