@@ -572,6 +572,10 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
 #define CKF_SPLIT_BLOCKS 4  // (measured: 3 -> 4 CTAs per SM, split 0.87 -> 0.79 ms at 2^28 slots)
 #endif
 constexpr int kSplitBlocks = CKF_SPLIT_BLOCKS;  // resident split CTAs per SM
+#ifndef CKF_SPLIT_PREFETCH
+#define CKF_SPLIT_PREFETCH 1
+#endif
+constexpr bool kSplitPrefetch = CKF_SPLIT_PREFETCH;
 
 template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
@@ -602,6 +606,17 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
     const uint32_t cc = w.cnt1[(size_t)c * kCntStride];
     const uint64_t cnt = cc < pl.cap1 ? cc : pl.cap1;
     if (off0 >= cnt) continue;  // block-uniform
+    if (kSplitPrefetch && threadIdx.x == 0) {  // this CTA's next tile into L2 (its records are a stream)
+      const uint64_t sn = s + gridDim.x;
+      if (sn < tiles) {
+        const uint32_t cn = (uint32_t)(sn / tiles_per_bin);
+        const uint64_t on = (sn % tiles_per_bin) * (uint64_t)kBTile;
+        if (on < pl.cap1) {
+          const uint64_t len = min((uint64_t)kBTile, pl.cap1 - on) & ~1ull;
+          if (len) prefetch_l2(w.bin1 + cn * pl.cap1 + on, (uint32_t)(len * 8));
+        }
+      }
+    }
     bin_release();
     for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.cnt[r] = 0;
     const uint64_t* src = w.bin1 + c * pl.cap1 + off0;
