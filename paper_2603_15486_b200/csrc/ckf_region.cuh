@@ -248,6 +248,21 @@ __device__ __forceinline__ bool smem_remove(uint32_t a, uint64_t tag, uint64_t (
   }
 }
 
+// One attempt of smem_insert / smem_remove: 0 = no candidate lane in the
+// snapshot, 1 = done, 2 = the CAS lost (the probe defers the record to a
+// compacted retry batch instead of re-running the whole warp's CAS body).
+template <bool kInsert, int F, int WPB>
+__device__ __forceinline__ int smem_try1(uint32_t a, uint64_t tag, const uint64_t (&w)[WPB]) {
+  constexpr int kTpw = 64 / F, kB = WPB * kTpw;
+  const int start = (int)(tag % kB) / kTpw;
+  const int slot = first_slot<F, WPB>(slot_mask<F, WPB>(w, kInsert ? 0ull : Lanes<F>::bcast(tag)), start);
+  if (slot < 0) return 0;
+  const int j = slot / kTpw, lane = slot % kTpw;
+  const uint64_t bw = pick<WPB>(w, j);
+  const uint64_t nw = kInsert ? bw | (tag << (lane * F)) : bw & ~(Lanes<F>::kLaneMask << (lane * F));
+  return cas_shared(a + 8u * j, bw, nw) == bw ? 1 : 2;
+}
+
 // Region-schedule results start all-true; only keys that end up negative /
 // not deleted cost a (random, L2-resident) bitmap update.
 __device__ __forceinline__ void clear_bit(uint32_t* bits, uint32_t i) { atomicAnd(bits + (i >> 5), ~(1u << (i & 31))); }
@@ -670,7 +685,8 @@ constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (307
 constexpr int kPStages = 3;
 template <int WPB>
 constexpr int kPSub = (16 / WPB) < kPPerLane ? (16 / WPB) : kPPerLane;  // records in flight per lane
-constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + 128;
+constexpr int kPRetry = 64;  // per-warp ring of deferred mutation records (power of two, >= 2 * 32)
+constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + kPWarps * kPRetry * 8 + 128;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
@@ -727,7 +743,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
   extern __shared__ __align__(128) uint8_t dsm[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(dsm);
   uint64_t* ring = reinterpret_cast<uint64_t*>(dsm + kRegionSmem);
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8);
+  uint64_t* retry = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8);  // [kPWarps][kPRetry]
+  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8 + kPWarps * kPRetry * 8);
   uint64_t* empty = full + kPStages;
   uint64_t* tbar = empty + kPStages;
   __shared__ uint32_t s_miss[1];
@@ -800,6 +817,71 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint32_t rn = next_region(r + gridDim.x);
       if (rn < pl.R) prefetch_l2(words + ((uint64_t)rn << pl.lrb) * WPB, region_buckets(rn) * bbytes);
     };
+    // Per-step epilogue of unresolved records (K of them per lane): phase 1
+    // misses go to this CTA's dense segment (warp reservation on a
+    // shared-memory counter), re-binned by alternate bucket for phase 2;
+    // phase-2 inserts still unplaced go to the eviction queue.  Whole warp.
+    auto settle = [&](uint32_t nm, const auto& rcs, const auto& i2s) {
+      constexpr int KK = sizeof(rcs) / sizeof(rcs[0]);
+      (void)KK;
+      if constexpr (PHASE == 1) {
+        const uint32_t c = __popc(nm);
+        n_alt += c;
+        uint32_t incl = c;
+#pragma unroll
+        for (int d = 1; d < 32; d <<= 1) {
+          const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
+          if (lane >= d) incl += y;
+        }
+        const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
+        if (total) {
+          uint32_t base = 0;
+          if (lane == 31) base = atomicAdd(s_miss, total);
+          base = __shfl_sync(0xffffffffu, base, 31);
+          uint4* dst = w.miss + (uint64_t)blockIdx.x * w.seg + base + incl - c;
+#pragma unroll
+          for (int q = 0; q < KK; ++q)
+            if ((nm >> q) & 1u)
+              *dst++ = make_uint4(ridx(rcs[q], pl.ish), (uint32_t)(rcs[q] & fpmask), (uint32_t)i2s[q],
+                                  (uint32_t)(i2s[q] >> 32));
+        }
+      } else if constexpr (OP == OP_INSERT && PHASE == 2) {
+        enqueue_evict_batch<KK>(sk, nm, rcs, pl.ish);
+      }
+    };
+    // Mutations whose single CAS attempt lost wait in this warp's retry ring
+    // and are resolved 32 at a time with the full loop (a lost CAS no longer
+    // re-runs the CAS body for the whole warp).  Warp-uniform head / count.
+    uint64_t* wring = retry + warp * kPRetry;
+    uint32_t rhead = 0, rcount = 0;
+    auto drain = [&](uint32_t mcnt, uint64_t b0r) {  // whole warp, mcnt <= 32
+      uint64_t rr[1];
+      uint64_t i2r[1] = {0};
+      uint32_t nm1 = 0;
+      rr[0] = lane < mcnt ? wring[(rhead + lane) & (kPRetry - 1)] : kFiller;
+      __syncwarp();
+      rhead += mcnt;
+      rcount -= mcnt;
+      if (lane < mcnt) {
+        const uint32_t loc = (uint32_t)(rr[0] >> pl.pb) & (rb - 1u);
+        const uint64_t fp = rr[0] & fpmask;
+        const uint32_t a = tab_a + loc * bbytes;
+        const uint64_t tag = PHASE == 1 ? fp : (POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp);
+        uint64_t wv1[WPB];
+        lds_bucket<WPB>(a, wv1);
+        const bool done = OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv1) : smem_remove<F, WPB>(a, tag, wv1);
+        n_ok += done;
+        if (OP == OP_DELETE && PHASE == 2 && !done) clear_bit(sk.bits, ridx(rr[0], pl.ish));
+        if (!done) {
+          nm1 = 1u;
+          if constexpr (PHASE == 1) {
+            uint64_t cc;
+            i2r[0] = alt_index<POL>(b0r + loc, fp, 0, g, cc);
+          }
+        }
+      }
+      settle(nm1, rr, i2r);
+    };
     uint32_t r = next_region(blockIdx.x);
     if (tid == 0 && r < pl.R) load_table(r);
     uint32_t cseq = 0, tpar = 0;
@@ -830,7 +912,8 @@ __global__ void __launch_bounds__(kPThreads, 1)
             // before their CAS (a stale snapshot costs a whole-warp retry)
             if (OP == OP_QUERY && v) lds_bucket_spread<WPB>(tab_a + loc * bbytes, wv[q]);
           }
-          uint32_t nm = 0;  // bit q: record q not resolved here
+          uint32_t nm = 0;     // bit q: record q not resolved here
+          uint32_t defer = 0;  // bit q: record q's CAS lost (mutations)
           uint64_t i2[K];
 #pragma unroll
           for (int q = 0; q < K; ++q) {
@@ -853,8 +936,12 @@ __global__ void __launch_bounds__(kPThreads, 1)
               const uint32_t a = tab_a + loc * bbytes;
               const uint64_t tag = PHASE == 1 ? fp : (POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp);
               lds_bucket<WPB>(a, wv[q]);  // (spread order measured slower here: instruction-bound)
-              const bool done =
-                  OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv[q]) : smem_remove<F, WPB>(a, tag, wv[q]);
+              const int r1 = smem_try1<OP == OP_INSERT, F, WPB>(a, tag, wv[q]);
+              if (r1 == 2) {  // lost CAS: resolved later in a compacted retry batch
+                defer |= 1u << q;
+                continue;
+              }
+              const bool done = r1 == 1;
               n_ok += done;
               if (OP == OP_DELETE && PHASE == 2 && !done) clear_bit(sk.bits, idx);  // tag in neither bucket
               if (!done) {
@@ -866,37 +953,29 @@ __global__ void __launch_bounds__(kPThreads, 1)
               }
             }
           }
-          if constexpr (PHASE == 1) {
-            // misses go to this CTA's dense segment (warp reservation on a
-            // shared-memory counter), re-binned by alternate bucket for phase 2
-            const uint32_t c = __popc(nm);
-            n_alt += c;
-            uint32_t incl = c;
+          settle(nm, rc, i2);
+          if constexpr (kMut) {
 #pragma unroll
-            for (int d = 1; d < 32; d <<= 1) {
-              const uint32_t y = __shfl_up_sync(0xffffffffu, incl, d);
-              if (lane >= d) incl += y;
+            for (int q = 0; q < K; ++q) {
+              const unsigned bal = __ballot_sync(0xffffffffu, (defer >> q) & 1u);
+              if (bal) {
+                if ((defer >> q) & 1u)
+                  wring[(rhead + rcount + __popc(bal & ((1u << lane) - 1u))) & (kPRetry - 1)] = rc[q];
+                rcount += __popc(bal);
+                __syncwarp();
+                if (rcount >= 32) drain(32, b0);
+              }
             }
-            const uint32_t total = __shfl_sync(0xffffffffu, incl, 31);
-            if (total) {
-              uint32_t base = 0;
-              if (lane == 31) base = atomicAdd(s_miss, total);
-              base = __shfl_sync(0xffffffffu, base, 31);
-              uint4* dst = w.miss + (uint64_t)blockIdx.x * w.seg + base + incl - c;
-#pragma unroll
-              for (int q = 0; q < K; ++q)
-                if ((nm >> q) & 1u)
-                  *dst++ = make_uint4(ridx(rc[q], pl.ish), (uint32_t)(rc[q] & fpmask), (uint32_t)i2[q],
-                                      (uint32_t)(i2[q] >> 32));
-            }
-          } else if constexpr (OP == OP_INSERT && PHASE == 2) {
-            enqueue_evict_batch<K>(sk, nm, rc, pl.ish);
           }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(empty + s);  // this warp is done with stage s
       }
-      // region boundary: write the slice back, bring in the next one
+      // region boundary: resolve this warp's deferred records, write the
+      // slice back, bring in the next one
+      if constexpr (kMut) {
+        while (rcount) drain(rcount < 32 ? rcount : 32, b0);
+      }
       if (kMut) fence_async_smem();  // this thread's shared-memory CASes before the bulk copy
       consumers_sync();
       if constexpr (OP == OP_INSERT) {
