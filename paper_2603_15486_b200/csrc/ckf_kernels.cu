@@ -676,7 +676,8 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   if (wpb != 1 && wpb != 2 && wpb != 4 && wpb != 8) return pl;
   const uint64_t m = p->bucket_count;
   const uint32_t pb = p->payload_bits;
-  if (pb > 24 || m < 2 || m > (1ull << 32) || n == 0) return pl;
+  if (pb > 32 || m < 2 || m > (1ull << 32) || n == 0) return pl;
+  const bool wide = pb > 24;  // f = 32: 16-byte records (RecT)
   const uint64_t bbytes = wpb * 8ull;
   uint32_t lrb = 0;
   const uint64_t smem = env_u64("CKF_REGION_KB", kRegionSmem >> 10) << 10;
@@ -694,6 +695,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   // index bit in the record)
   const uint64_t per_rec = op == CKF_OP_QUERY ? 2 : 1;
   auto runs_for = [&](uint32_t lrbc_) -> uint64_t {
+    if (wide) return 1;
     uint64_t km = (1ull << (64 - (pb + lrbc_ + 1))) - 2;
     if (km > (1ull << 31) / per_rec) km = (1ull << 31) / per_rec;
     return (n + km - 1) / km;
@@ -705,11 +707,11 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   if (lrbc - lrb > ceil_log2(kMaxF2)) return pl;
   const uint64_t R1 = (m + (1ull << lrbc) - 1) >> lrbc;
   if (R1 > (uint64_t)kRMaxCoarse) return pl;
-  const uint32_t ish = pb + lrbc + 1;
-  if (ish > 62) return pl;
+  const uint32_t ish = wide ? 32 : pb + lrbc + 1;  // (unused by 16-byte records)
+  if (ish > 62 || (wide && lrbc > 31)) return pl;
   // keys per run: the index field (all-ones is the filler), 32-bit miss-entry
   // indices, and < 2^32 record slots over the coarse bins (dual query records)
-  uint64_t kmax = (1ull << (64 - ish)) - 2;
+  uint64_t kmax = wide ? ~0ull : (1ull << (64 - ish)) - 2;
   if (kmax > (1ull << 31) / per_rec) kmax = (1ull << 31) / per_rec;
   const uint64_t kenv = env_u64("CKF_MAX_RUN_KEYS", 0);  // developer knob: exercise multi-run calls
   if (kenv && kenv < kmax) kmax = kenv;
@@ -722,6 +724,7 @@ static RPlan make_rplan(const ckf_params* p, uint64_t n, int op, unsigned flags,
   pl.R = pl.R1 * pl.F2;
   pl.pb = pb;
   pl.ish = ish;
+  pl.rbytes = wide ? 16 : 8;
   const double recs = (double)pl.chunk * (double)per_rec;
   // + run padding: at most one filler per bin per tile of the pass that fills it
   // (bin: ceil(chunk / tile) tiles + one partial tile per miss segment; split: a coarse bin's tiles)
@@ -757,8 +760,8 @@ static RLayout rlayout_for(const RPlan& pl, int op) {
   L.qstart = L.ctr_end;  // insert: eviction-queue length before this run (not zeroed per run)
   L.room = align256(L.qstart + 16);  // insert: [qstart, eviction cursor], then the room bit per bucket
   L.bin1 = align256(L.room + (op == CKF_OP_INSERT ? ((uint64_t)pl.R << pl.lrb) / 8 : 0));
-  L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * 8);
-  L.miss = align256(L.binf + pl.R * pl.capf * 8);
+  L.binf = align256(L.bin1 + pl.R1 * pl.cap1 * pl.rbytes);
+  L.miss = align256(L.binf + pl.R * pl.capf * pl.rbytes);
   L.bits = align256(L.miss + probe_grid(pl) * miss_seg(pl) * 16);
   L.total = align256(L.bits + (op == CKF_OP_INSERT ? 0 : (pl.chunk + 31) / 32 * 4));
   return L;
@@ -771,8 +774,8 @@ static RWork rwork_view(void* ws, const RLayout& L, const RPlan& pl) {
   w.cntf = (uint32_t*)(b + L.cntf);
   w.n_miss = (uint32_t*)(b + L.n_miss);
   w.mode = (uint32_t*)(b + L.mode);
-  w.bin1 = (uint64_t*)(b + L.bin1);
-  w.binf = (uint64_t*)(b + L.binf);
+  w.bin1 = b + L.bin1;
+  w.binf = b + L.binf;
   w.miss = (uint4*)(b + L.miss);
   w.bits = (uint32_t*)(b + L.bits);
   w.room = (uint32_t*)(b + L.room);
@@ -819,12 +822,13 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   long long* mocc = OP == OP_QUERY ? nullptr : occ;
   const int sms = sm_count();
   const unsigned pg = probe_grid(pl);
-  constexpr uint32_t kBinSmem = sizeof(BinSmem);
+  constexpr uint32_t kBinSmem = sizeof(BinSmem<F>);
+  constexpr uint32_t kProbeSmemF = kProbeSmem<F>;
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
   allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmem);
-  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmem);
-  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmem);
+  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmemF);
+  allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmemF);
   int st;
   // phase 1: primary buckets
   region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, kBinBlocks), kBThreads, kBinSmem, s>>>(
@@ -832,7 +836,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   if ((st = status())) return st;
   region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
-  region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
+  region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   // phase 2: the misses, on their alternate buckets
   if (cudaMemsetAsync(ws, 0, L.bin_ctr_end, s) != cudaSuccess) return cuda_error();
@@ -841,7 +845,7 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   if ((st = status())) return st;
   region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
-  region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmem, s>>>(g, pl, words, w, sk, mocc);
+  region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   if (OP != OP_INSERT) {
     expand_count_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out,
@@ -880,7 +884,7 @@ struct QueryArgs {
 template <int F, int WPB, int POL>
 struct QueryOp {
   static int run(const QueryArgs& a) {
-    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr (WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.region) {
         for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
           uint64_t off, cnt;
@@ -947,7 +951,7 @@ struct InsertOp {
                                                    a.occ, a.hashed);
       return status();
     }
-    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr (WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.region && a.cap) {
         // every key counts as stored until the eviction pass says otherwise
         if (cudaMemsetAsync(a.ok, 1, a.n, a.s) != cudaSuccess) return cuda_error();
@@ -1001,7 +1005,7 @@ struct DeleteOp {
       seq_delete_kernel<F, POL><<<1, 1, 0, a.s>>>(a.g, a.words, a.keys, a.n, a.out, a.ctr, a.occ, a.hashed);
       return status();
     }
-    if constexpr ((WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) && F != 32) {
+    if constexpr (WPB == 1 || WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.region) {
         for (uint64_t k = 0, nr = run_count(a.t, a.n); k < nr; ++k) {
           uint64_t off, cnt;
@@ -1433,13 +1437,23 @@ int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* f
 // Schedule of one call: the region schedule when its plan applies and the
 // caller's workspace holds it, else the direct kernels.  Automatic choice:
 // tables past the L2 (>= 48 MiB) and at least one key per bucket.
-static bool region_wanted(const ckf_params* p, uint64_t n, unsigned flags) {
+// The batch size from which the region schedule beats the direct kernels, in
+// keys per bucket (measured on a 2^28-slot table, profiles/r02_crossover.jsonl):
+// 32-byte buckets cross over at ~1 key per bucket for insert / delete /
+// lookup- and ~2-3 for lookup+ (the direct lookup of a mostly-positive batch
+// reads one sector per key); 64-byte buckets (f = 32) at ~1.5 for every op.
+static double region_threshold(const ckf_params* p, int op) {
+  if (p->words_per_bucket >= 8) return 1.5;
+  return op == CKF_OP_QUERY ? 2.0 : 1.0;
+}
+
+static bool region_wanted(const ckf_params* p, uint64_t n, int op, unsigned flags) {
   if (flags & (CKF_FORCE_DIRECT | CKF_MODE_SEQUENTIAL)) return false;
   if (n == 0) return false;
   if (!(flags & CKF_FORCE_TILED)) {
     if (!env_u64("CKF_TILED_AUTO", 1)) return false;
     const uint64_t table = p->bucket_count * p->words_per_bucket * 8ull;
-    if (table < kRegionMinTable || n < p->bucket_count) return false;
+    if (table < kRegionMinTable || (double)n < region_threshold(p, op) * (double)p->bucket_count) return false;
   }
   return true;
 }
@@ -1447,7 +1461,7 @@ static bool region_wanted(const ckf_params* p, uint64_t n, unsigned flags) {
 static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys, void* ws,
                         uint64_t ws_bytes) {
   TiledArgs t{};
-  if (!ws || !region_wanted(p, n, flags) || ((uintptr_t)keys % 8) != 0 || ((uintptr_t)ws % 256) != 0) return t;
+  if (!ws || !region_wanted(p, n, op, flags) || ((uintptr_t)keys % 8) != 0 || ((uintptr_t)ws % 256) != 0) return t;
   bool ok = false;
   t.rpl = make_rplan(p, n, op, flags, ok);
   if (!ok) return t;
@@ -1458,11 +1472,7 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
 }
 
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
-  if (!params_ok(p) || !region_wanted(p, n, flags)) return 0;
-  if (op == CKF_OP_INSERT || op == CKF_OP_DELETE || op == CKF_OP_QUERY) {
-    const uint32_t f = p->fingerprint_bits, wpb = p->words_per_bucket;
-    if (f == 32 || (wpb != 1 && wpb != 2 && wpb != 4 && wpb != 8)) return 0;
-  }
+  if (!params_ok(p) || !region_wanted(p, n, op, flags)) return 0;
   bool ok;
   const RPlan rp = make_rplan(p, n, op, flags, ok);
   return ok ? rlayout_for(rp, op).total : 0;

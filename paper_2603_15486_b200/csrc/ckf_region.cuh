@@ -130,7 +130,9 @@ __device__ __forceinline__ uint32_t lane_mask(uint64_t x) {
   const uint32_t zl = zind32<F>((uint32_t)x), zh = zind32<F>((uint32_t)(x >> 32));
   // indicators at bit 7 of bytes 0..3 -> bits 28..31 (no carries: all partial
   // products land on distinct bits)
-  if constexpr (F == 16) {
+  if constexpr (F == 32) {
+    return (zl >> 31) | ((zh >> 31) << 1);
+  } else if constexpr (F == 16) {
     return (__byte_perm(zl, zh, 0x7531) * 0x00204081u) >> 28;
   } else {
     return ((zl * 0x00204081u) >> 28) | (((zh * 0x00204081u) >> 28) << 4);
@@ -287,21 +289,68 @@ struct RPlan {
   uint32_t lrb;      // log2 buckets per fine region
   uint32_t R;        // fine regions = R1 * F2 (the last ones may be empty)
   uint32_t pb;       // fingerprint bits in a record
-  uint32_t ish;      // index shift: pb + lrbc + 1
+  uint32_t ish;      // index shift: pb + lrbc + 1 (8-byte records)
   uint64_t chunk;    // keys per region run (a call of n > chunk keys runs ceil(n / chunk) of them)
+  uint32_t rbytes;   // record bytes: 8, or 16 for f = 32 (RecT)
 };
 
-__device__ __forceinline__ uint64_t rpack(uint64_t idx, uint32_t alt, uint64_t off, uint64_t fp, const RPlan& pl) {
-  return (idx << pl.ish) | ((uint64_t)alt << (pl.ish - 1)) | (off << pl.pb) | fp;
-}
-__device__ __forceinline__ uint32_t ridx(uint64_t rc, uint32_t ish) { return (uint32_t)(rc >> ish); }
-__device__ __forceinline__ uint32_t ralt(uint64_t rc, uint32_t ish) { return (uint32_t)(rc >> (ish - 1)) & 1u; }
+// 16-byte record of f = 32 filters, whose 32-bit fingerprint leaves no room
+// for an index in 64 bits: lo = offset in its region << 32 | fp, hi = index <<
+// 1 | alt; hi all ones = filler.
+struct __align__(16) Rec16 {
+  uint64_t lo, hi;
+};
+
+// The record of an f-bit filter and its fields.  8 B for f <= 16 (the
+// default, layout above), 16 B for f = 32.
+template <int F>
+struct RecT {
+  static constexpr bool kWide = F == 32;
+  using T = typename std::conditional<kWide, Rec16, uint64_t>::type;
+  static constexpr uint32_t kBytes = sizeof(T);
+  static constexpr bool kPadEven = !kWide;  // bulk copies move 16 B granules: 8 B runs pad to even length
+  static __device__ __forceinline__ T pack(uint64_t idx, uint32_t alt, uint64_t off, uint64_t fp, const RPlan& pl) {
+    if constexpr (kWide) return Rec16{(off << 32) | fp, (idx << 1) | alt};
+    else return (idx << pl.ish) | ((uint64_t)alt << (pl.ish - 1)) | (off << pl.pb) | fp;
+  }
+  static __device__ __forceinline__ uint32_t idx(const T& r, const RPlan& pl) {
+    if constexpr (kWide) return (uint32_t)(r.hi >> 1);
+    else return (uint32_t)(r >> pl.ish);
+  }
+  static __device__ __forceinline__ uint32_t alt(const T& r, const RPlan& pl) {
+    if constexpr (kWide) return (uint32_t)r.hi & 1u;
+    else return (uint32_t)(r >> (pl.ish - 1)) & 1u;
+  }
+  // the offset field (bucket in the record's region) masked to `mask`
+  static __device__ __forceinline__ uint32_t off(const T& r, const RPlan& pl, uint32_t mask) {
+    if constexpr (kWide) return (uint32_t)(r.lo >> 32) & mask;
+    else return (uint32_t)(r >> pl.pb) & mask;
+  }
+  static __device__ __forceinline__ uint64_t fp(const T& r, const RPlan& pl) {
+    if constexpr (kWide) return r.lo & 0xFFFFFFFFull;
+    else return r & ((1ull << pl.pb) - 1u);
+  }
+  // coarse record -> fine record: drop the offset bits above the fine region
+  static __device__ __forceinline__ T refine(const T& r, const RPlan& pl) {
+    const uint64_t drop = (uint64_t)((1u << (pl.lrbc - pl.lrb)) - 1u) << pl.lrb;
+    if constexpr (kWide) return Rec16{r.lo & ~(drop << 32), r.hi};
+    else return r & ~(drop << pl.pb);
+  }
+  static __device__ __forceinline__ T filler() {
+    if constexpr (kWide) return Rec16{~0ull, ~0ull};
+    else return ~0ull;
+  }
+  static __device__ __forceinline__ bool is_filler(const T& r) {
+    if constexpr (kWide) return r.hi == ~0ull;
+    else return r == ~0ull;
+  }
+};
 
 struct RWork {
   uint32_t* cnt1;   // [R1 * kCntStride] coarse bin fill
   uint32_t* cntf;   // [R * kCntStride] fine bin fill
-  uint64_t* bin1;   // [R1 * cap1] coarse bins
-  uint64_t* binf;   // [R * capf] fine bins
+  void* bin1;       // [R1 * cap1] coarse bins of records (RecT)
+  void* binf;       // [R * capf] fine bins
   uint4* miss;      // [grid * seg] per-probe-CTA dense segments of phase-1 misses {idx, fp, i2 lo, i2 hi}
   uint32_t* n_miss; // [grid] entries per segment
   uint64_t seg;     // entries per segment
@@ -316,13 +365,14 @@ struct RWork {
 // resolve it in place on the global table -- legal here because no region is
 // resident in shared memory while the bin / split kernels run.
 template <int OP, int F, int WPB, int POL>
-__device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, uint32_t ish, uint64_t rec,
-                                               uint64_t bucket, const Sink& sk, const uint32_t* w_mode,
-                                               uint32_t& n_ok, uint32_t& n_alt) {
+__device__ __forceinline__ void resolve_direct(uint64_t* words, const Geo& g, const RPlan& pl,
+                                               const typename RecT<F>::T& rec, uint64_t bucket, const Sink& sk,
+                                               const uint32_t* w_mode, uint32_t& n_ok, uint32_t& n_alt) {
   using Lg = Logic<OP, F, WPB, POL>;
-  const uint32_t idx = ridx(rec, ish);
-  const uint64_t fp = rec & ((1ull << g.payload_bits) - 1u);
-  const bool phase2 = ralt(rec, ish);  // the record is of the key's alternate bucket
+  using RT = RecT<F>;
+  const uint32_t idx = RT::idx(rec, pl);
+  const uint64_t fp = RT::fp(rec, pl);
+  const bool phase2 = RT::alt(rec, pl);  // the record is of the key's alternate bucket
   uint64_t c;
   bool done;
   if (phase2) {
@@ -357,20 +407,21 @@ constexpr int kBTile = kBThreads * kBItems;  // records per tile
 // length is padded with one filler record (all ones: its index field would be
 // 2^(64-ish) - 1, never a key, as a run holds < 2^(64-ish) - 1 keys) that every
 // consumer skips.
-constexpr uint64_t kFiller = ~0ull;
-__device__ __forceinline__ bool is_filler(uint64_t rc) { return rc == kFiller; }
-
-struct BinSmem {
-  uint64_t rec[kBTile + kRMaxCoarse];  // sorted tile (bulk writer: runs padded to even length)
+template <class T>
+struct BinSmemT {
+  T rec[kBTile + kRMaxCoarse];         // sorted tile (8 B records: runs padded to even length)
   uint32_t cnt[kRMaxCoarse];           // records per bin in this tile
-  uint2 sg[kRMaxCoarse];               // {run start in rec, run start in the bin} (bulk: both even)
+  uint2 sg[kRMaxCoarse];               // {run start in rec, run start in the bin}
   uint32_t warp_sums[kBThreads / 32];
 };
+template <int F>
+using BinSmem = BinSmemT<typename RecT<F>::T>;
 
 // sm.cnt (records per bin) -> sm.sg.x (exclusive scan of the padded run
 // lengths) and sm.sg.y (one global reservation per non-empty bin)
-template <bool kBulk>
-__device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem& sm) {
+template <int F>
+__device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem<F>& sm) {
+  constexpr bool kBulk = RecT<F>::kPadEven;
   constexpr int NW = kBThreads / 32;
   const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
   const uint32_t per = (nb + kBThreads - 1) / kBThreads;  // <= 2
@@ -407,13 +458,14 @@ __device__ __forceinline__ void bin_reserve(uint32_t nb, uint32_t* gcnt, BinSmem
     const uint32_t r = lo + k;
     if (r < hi) {
       sm.sg[r] = make_uint2(run, gb[k]);
-      if (kBulk && (sm.cnt[r] & 1u)) sm.rec[run + sm.cnt[r]] = kFiller;
+      if (kBulk && (sm.cnt[r] & 1u)) sm.rec[run + sm.cnt[r]] = RecT<F>::filler();
       run += c[k];
     }
   }
 }
 
-__device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank, uint64_t rc) {
+template <class T>
+__device__ __forceinline__ void bin_place(BinSmemT<T>& sm, uint32_t b, uint32_t rank, const T& rc) {
   sm.rec[sm.sg[b].x + rank] = rc;
 }
 
@@ -421,29 +473,31 @@ __device__ __forceinline__ void bin_place(BinSmem& sm, uint32_t b, uint32_t rank
 // not fit its bin (adversarial inputs only) goes record by record: the part
 // that fits by plain stores, the rest to ovf(rec, bin).  Caller: all threads,
 // after bin_place; shared memory is released by bin_release().
-template <class Ovf>
-__device__ __forceinline__ void bin_write(uint32_t nb, uint64_t* __restrict__ out, uint64_t cap, BinSmem& sm,
-                                          Ovf&& ovf) {
+template <int F, class Ovf>
+__device__ __forceinline__ void bin_write(uint32_t nb, typename RecT<F>::T* __restrict__ out, uint64_t cap,
+                                          BinSmem<F>& sm, Ovf&& ovf) {
+  using RT = RecT<F>;
+  using T = typename RT::T;
   fence_async_smem();  // this thread's placements -> visible to the bulk copies
   __syncthreads();
   bool issued = false;
   for (uint32_t r = threadIdx.x; r < nb; r += kBThreads) {
     const uint32_t c = sm.cnt[r];
     if (!c) continue;
-    const uint32_t cr = (c + 1u) & ~1u, st = sm.sg[r].x, gb = sm.sg[r].y;
-    uint64_t* dst = out + (uint64_t)r * cap;
+    const uint32_t cr = RT::kPadEven ? (c + 1u) & ~1u : c, st = sm.sg[r].x, gb = sm.sg[r].y;
+    T* dst = out + (uint64_t)r * cap;
     if ((uint64_t)gb + cr <= cap) {
       asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(dst + gb),
-                   "r"(saddr(&sm.rec[st])), "r"(cr * 8u)
+                   "r"(saddr(&sm.rec[st])), "r"(cr * RT::kBytes)
                    : "memory");
       issued = true;
     } else {
       for (uint32_t k = 0; k < c; ++k) {
-        const uint64_t rc = sm.rec[st + k];
+        const T rc = sm.rec[st + k];
         if ((uint64_t)gb + k < cap) dst[gb + k] = rc;
         else ovf(rc, r);
       }
-      if ((c & 1u) && (uint64_t)gb + c < cap) dst[gb + c] = kFiller;
+      if (RT::kPadEven && (c & 1u) && (uint64_t)gb + c < cap) dst[gb + c] = RT::filler();
     }
   }
   if (issued) asm volatile("cp.async.bulk.commit_group;" ::: "memory");
@@ -467,8 +521,10 @@ template <int OP, int F, int WPB, int POL, int SRC>
 __global__ void __launch_bounds__(kBThreads, kBinBlocks)
     region_bin_kernel(Geo g, RPlan pl, uint64_t* words, const uint64_t* __restrict__ keys, uint64_t n_keys, bool hashed,
                       RWork w, Sink sk, long long* occ) {
-  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
-  BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
+  using RT = RecT<F>;
+  using T = typename RT::T;
+  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem<F>), dynamic (> 48 KiB)
+  BinSmem<F>& sm = *reinterpret_cast<BinSmem<F>*>(bsm_raw);
   // dual: a query batch sampled as mostly negative gets an i1 AND an i2 record
   // per key here (no phase 2); the tile then holds kBTile / 2 keys
   const bool dual = OP == OP_QUERY && SRC == SRC_KEYS && w.mode[0] == 0;
@@ -490,7 +546,7 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
     }
     bin_release();
     for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.cnt[r] = 0;
-    uint64_t rec[kBItems];
+    T rec[kBItems];
     uint32_t pk[kBItems];  // bin << 16 | rank; 0xFFFFFFFF = no record
     if constexpr (SRC == SRC_KEYS) {
       // item q of thread t: key t0 + (q / 2) * 2 * kBThreads + 2t + (q % 2) (pairs
@@ -529,13 +585,21 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
         const uint64_t fp = fp0 ? fp0 : 1u;
         const uint64_t i1 = POL == CKF_POLICY_XOR ? (h & g.mask) : reduce_index(h & 0xFFFFFFFFull, g);
         const uint32_t b1 = (uint32_t)i1 >> pl.lrbc;
-        rec[q] = ixq | ((uint64_t)((uint32_t)i1 & lmask) << pl.pb) | fp;
+        if constexpr (RT::kWide)
+          rec[q] = RT::pack(t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1), 0u,
+                            (uint32_t)i1 & lmask, fp, pl);
+        else
+          rec[q] = ixq | ((uint64_t)((uint32_t)i1 & lmask) << pl.pb) | fp;
         pk[q] = mine ? (b1 << 16) | atomicAdd(&sm.cnt[b1], 1u) : 0xFFFFFFFFu;
         if (q < kBItems / 2 && dual) {
           uint64_t cc;
           const uint64_t i2 = alt_index<POL>(i1, fp, 0, g, cc);
           const uint32_t b2 = (uint32_t)i2 >> pl.lrbc;
-          rec[q + kBItems / 2] = ixq | alt1 | ((uint64_t)((uint32_t)i2 & lmask) << pl.pb) | fp;
+          if constexpr (RT::kWide)
+            rec[q + kBItems / 2] = RT::pack(t0 + (uint64_t)(q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1), 1u,
+                                            (uint32_t)i2 & lmask, fp, pl);
+          else
+            rec[q + kBItems / 2] = ixq | alt1 | ((uint64_t)((uint32_t)i2 & lmask) << pl.pb) | fp;
           pk[q + kBItems / 2] = mine ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
         if (q & 1) ix += s2;
@@ -555,7 +619,7 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
           const uint64_t i = t0 + (uint64_t)(q0 + q) * kBThreads + threadIdx.x;
           const uint64_t i2 = (uint64_t)e[q].z | ((uint64_t)e[q].w << 32);
           const uint32_t b2 = (uint32_t)(i2 >> pl.lrbc);
-          rec[q0 + q] = rpack(e[q].x, 1u, i2 & lmask, e[q].y, pl);
+          rec[q0 + q] = RT::pack(e[q].x, 1u, i2 & lmask, e[q].y, pl);
           pk[q0 + q] = i < n ? (b2 << 16) | atomicAdd(&sm.cnt[b2], 1u) : 0xFFFFFFFFu;
         }
       }
@@ -563,16 +627,16 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
     __syncthreads();
     // runs leave as bulk copies (measured at 16-record runs: 1.46 vs 1.49 ms
     // for per-record coalesced stores, which also need a slot array)
-    bin_reserve<true>(pl.R1, w.cnt1, sm);
+    bin_reserve<F>(pl.R1, w.cnt1, sm);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
       if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q]);
-    auto ovf = [&](uint64_t rc, uint32_t b) {
-      const uint64_t bucket = ((uint64_t)b << pl.lrbc) + ((rc >> pl.pb) & lmask);
-      resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
+    auto ovf = [&](const T& rc, uint32_t b) {
+      const uint64_t bucket = ((uint64_t)b << pl.lrbc) + RT::off(rc, pl, lmask);
+      resolve_direct<OP, F, WPB, POL>(words, g, pl, rc, bucket, sk, w.mode, n_ok, n_alt);
     };
-    bin_write(pl.R1, w.bin1, pl.cap1, sm, ovf);
+    bin_write<F>(pl.R1, reinterpret_cast<T*>(w.bin1), pl.cap1, sm, ovf);
     __syncthreads();
   }
   bulk_wait_all();
@@ -595,8 +659,11 @@ constexpr bool kSplitPrefetch = CKF_SPLIT_PREFETCH;
 template <int OP, int F, int WPB, int POL>
 __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
     region_split_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
-  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem), dynamic (> 48 KiB)
-  BinSmem& sm = *reinterpret_cast<BinSmem*>(bsm_raw);
+  using RT = RecT<F>;
+  using T = typename RT::T;
+  extern __shared__ __align__(16) uint8_t bsm_raw[];  // sizeof(BinSmem<F>), dynamic (> 48 KiB)
+  BinSmem<F>& sm = *reinterpret_cast<BinSmem<F>*>(bsm_raw);
+  const T* bin1 = reinterpret_cast<const T*>(w.bin1);
   const uint64_t pol = evict_first_policy();
   // tiles per coarse bin from the fullest bin of THIS pass (phase 2 bins hold
   // ~10 % of phase 1's records: no walk over the empty tail of every bin)
@@ -611,9 +678,7 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
   const uint64_t maxcnt = s_max < pl.cap1 ? s_max : pl.cap1;
   const uint32_t tiles_per_bin = (uint32_t)((maxcnt + kBTile - 1) / kBTile);
   const uint64_t tiles = (uint64_t)pl.R1 * tiles_per_bin;
-  const uint32_t fshift = pl.pb + pl.lrb;  // offset bits above the fine offset
   const uint32_t fmask = pl.F2 - 1u;
-  const uint64_t keep = ~((uint64_t)((1u << (pl.lrbc - pl.lrb)) - 1u) << fshift);  // clears the fine-region bits
   uint32_t n_ok = 0, n_alt = 0;
   for (uint64_t s = blockIdx.x; s < tiles; s += gridDim.x) {
     const uint32_t c = (uint32_t)(s / tiles_per_bin);
@@ -628,19 +693,28 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
         const uint64_t on = (sn % tiles_per_bin) * (uint64_t)kBTile;
         if (on < pl.cap1) {
           const uint64_t len = min((uint64_t)kBTile, pl.cap1 - on) & ~1ull;
-          if (len) prefetch_l2(w.bin1 + cn * pl.cap1 + on, (uint32_t)(len * 8));
+          if (len) prefetch_l2(bin1 + cn * pl.cap1 + on, (uint32_t)(len * RT::kBytes));
         }
       }
     }
     bin_release();
     for (uint32_t r = threadIdx.x; r < pl.F2; r += kBThreads) sm.cnt[r] = 0;
-    const uint64_t* src = w.bin1 + c * pl.cap1 + off0;
+    const T* src = bin1 + c * pl.cap1 + off0;
     const uint32_t nrec = (uint32_t)min((uint64_t)kBTile, cnt - off0);
-    uint64_t rec[kBItems];
+    T rec[kBItems];
 #pragma unroll
     for (int q = 0; q < kBItems / 2; ++q) {
       const uint32_t e = q * 2 * kBThreads + 2 * threadIdx.x;
-      if (e + 1 < nrec) {
+      if constexpr (RT::kWide) {  // two 16 B records: one 32 B load
+        if (e + 1 < nrec) {
+          asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v4.u64 {%0,%1,%2,%3}, [%4], %5;"
+                       : "=l"(rec[2 * q].lo), "=l"(rec[2 * q].hi), "=l"(rec[2 * q + 1].lo), "=l"(rec[2 * q + 1].hi)
+                       : "l"(src + e), "l"(pol));
+        } else {
+          rec[2 * q] = e < nrec ? src[e] : RT::filler();
+          rec[2 * q + 1] = RT::filler();
+        }
+      } else if (e + 1 < nrec) {
         asm volatile("ld.global.nc.L1::no_allocate.L2::cache_hint.v2.u64 {%0,%1}, [%2], %3;"
                      : "=l"(rec[2 * q]), "=l"(rec[2 * q + 1])
                      : "l"(src + e), "l"(pol));
@@ -654,18 +728,19 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
 #pragma unroll
     for (int q = 0; q < kBItems; ++q) {
       const uint32_t e = (q >> 1) * 2 * kBThreads + 2 * threadIdx.x + (q & 1);
-      const uint32_t f = (uint32_t)(rec[q] >> fshift) & fmask;
-      pk[q] = e < nrec && !is_filler(rec[q]) ? (f << 16) | atomicAdd(&sm.cnt[f], 1u) : 0xFFFFFFFFu;
+      const uint32_t f = (RT::off(rec[q], pl, 0xFFFFFFFFu) >> pl.lrb) & fmask;
+      pk[q] = e < nrec && !RT::is_filler(rec[q]) ? (f << 16) | atomicAdd(&sm.cnt[f], 1u) : 0xFFFFFFFFu;
     }
     __syncthreads();
-    bin_reserve<true>(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
+    bin_reserve<F>(pl.F2, w.cntf + (size_t)c * pl.F2 * kCntStride, sm);
     __syncthreads();
 #pragma unroll
     for (int q = 0; q < kBItems; ++q)
-      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, rec[q] & keep);
-    bin_write(pl.F2, w.binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](uint64_t rc, uint32_t f) {
-      const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + ((rc >> pl.pb) & ((1u << pl.lrb) - 1u));
-      resolve_direct<OP, F, WPB, POL>(words, g, pl.ish, rc, bucket, sk, w.mode, n_ok, n_alt);
+      if (pk[q] != 0xFFFFFFFFu) bin_place(sm, pk[q] >> 16, pk[q] & 0xFFFFu, RT::refine(rec[q], pl));
+    T* binf = reinterpret_cast<T*>(w.binf);
+    bin_write<F>(pl.F2, binf + (uint64_t)c * pl.F2 * pl.capf, pl.capf, sm, [&](const T& rc, uint32_t f) {
+      const uint64_t bucket = ((uint64_t)(c * pl.F2 + f) << pl.lrb) + RT::off(rc, pl, (1u << pl.lrb) - 1u);
+      resolve_direct<OP, F, WPB, POL>(words, g, pl, rc, bucket, sk, w.mode, n_ok, n_alt);
     });
     __syncthreads();
   }
@@ -680,13 +755,19 @@ __global__ void __launch_bounds__(kBThreads, kSplitBlocks)
 constexpr int kPWarps = 24;                     // consumer warps (measured: 16 and 30 slower)
 constexpr int kPConsumers = kPWarps * 32;
 constexpr int kPThreads = kPConsumers + 32;     // + one producer warp (<= 1024 threads)
-constexpr int kPPerLane = 4;                    // records per consumer lane per chunk
-constexpr int kPChunk = kPConsumers * kPPerLane;  // records per ring stage (3072)
+// records per consumer lane per chunk: 4 (8 B records), 2 (16 B: the ring
+// keeps its 72 KiB)
+template <int F>
+constexpr int kPPerLane = RecT<F>::kWide ? 2 : 4;
+template <int F>
+constexpr int kPChunk = kPConsumers * kPPerLane<F>;  // records per ring stage (3072 / 1536)
 constexpr int kPStages = 3;
-template <int WPB>
-constexpr int kPSub = (16 / WPB) < kPPerLane ? (16 / WPB) : kPPerLane;  // records in flight per lane
+template <int F, int WPB>
+constexpr int kPSub = (16 / WPB) < kPPerLane<F> ? (16 / WPB) : kPPerLane<F>;  // records in flight per lane
 constexpr int kPRetry = 64;  // per-warp ring of deferred mutation records (power of two, >= 2 * 32)
-constexpr uint32_t kProbeSmem = kRegionSmem + kPStages * kPChunk * 8 + kPWarps * kPRetry * 8 + 128;
+template <int F>
+constexpr uint32_t kProbeSmem =
+    kRegionSmem + (kPStages * kPChunk<F> + kPWarps * kPRetry) * RecT<F>::kBytes + 128;
 
 __device__ __forceinline__ void mbar_arrive(uint64_t* b) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
@@ -699,9 +780,9 @@ __device__ __forceinline__ void consumers_sync() { asm volatile("bar.sync 1, %0;
 // never waits on the scattered key reads.  Whole warp, converged.
 constexpr uint64_t kRehash = ~0ull;
 
-template <int K>
-__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const uint64_t (&rc)[K],
-                                                    uint32_t ish) {
+template <int F, int K>
+__device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm, const typename RecT<F>::T (&rc)[K],
+                                                    const RPlan& pl) {
   const int lane = threadIdx.x & 31;
   const uint32_t c = __popc(nm);
   uint32_t incl = c;
@@ -719,7 +800,7 @@ __device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm,
 #pragma unroll
   for (int q = 0; q < K; ++q) {
     if (!((nm >> q) & 1u)) continue;
-    const uint32_t idx = ridx(rc[q], ish);
+    const uint32_t idx = RecT<F>::idx(rc[q], pl);
     if (pos < sk.rec_cap) sk.rec[pos] = ckf_record{sk.ibase + idx, kRehash, 0u, 0u};
     else if (sk.ok) sk.ok[idx] = 0;
     ++pos;
@@ -740,17 +821,20 @@ __device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm,
 template <int OP, int F, int WPB, int POL, int PHASE>
 __global__ void __launch_bounds__(kPThreads, 1)
     region_probe_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
+  using RT = RecT<F>;
+  using T = typename RT::T;
+  constexpr int kPL = kPPerLane<F>, kCh = kPChunk<F>;
   extern __shared__ __align__(128) uint8_t dsm[];
   uint64_t* tab = reinterpret_cast<uint64_t*>(dsm);
-  uint64_t* ring = reinterpret_cast<uint64_t*>(dsm + kRegionSmem);
-  uint64_t* retry = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8);  // [kPWarps][kPRetry]
-  uint64_t* full = reinterpret_cast<uint64_t*>(dsm + kRegionSmem + kPStages * kPChunk * 8 + kPWarps * kPRetry * 8);
+  T* ring = reinterpret_cast<T*>(dsm + kRegionSmem);
+  T* retry = ring + kPStages * kCh;  // [kPWarps][kPRetry]
+  uint64_t* full = reinterpret_cast<uint64_t*>(retry + kPWarps * kPRetry);
   uint64_t* empty = full + kPStages;
   uint64_t* tbar = empty + kPStages;
   __shared__ uint32_t s_miss[1];
   constexpr bool kMut = OP != OP_QUERY;
   const uint32_t* cnt = w.cntf;
-  const uint64_t* bins = w.binf;
+  const T* bins = reinterpret_cast<const T*>(w.binf);
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rb = 1u << pl.lrb;
   constexpr uint32_t bbytes = WPB * 8;
@@ -782,19 +866,19 @@ __global__ void __launch_bounds__(kPThreads, 1)
       uint32_t iseq = 0;
       for (uint32_t r = blockIdx.x; r < pl.R; r += gridDim.x) {
         const uint32_t cn = region_count(r);
-        for (uint32_t k0 = 0; k0 < cn; k0 += kPChunk, ++iseq) {
+        for (uint32_t k0 = 0; k0 < cn; k0 += kCh, ++iseq) {
           const uint32_t s = iseq % kPStages;
           if (iseq >= (uint32_t)kPStages) mbar_wait(empty + s, ((iseq / kPStages) - 1u) & 1u);
-          const uint32_t len = min((uint32_t)kPChunk, cn - k0);
-          const uint32_t bytes = ((len + 1u) & ~1u) * 8u;  // bins are even-sized and 16 B aligned
+          const uint32_t len = min((uint32_t)kCh, cn - k0);
+          // bins are even-sized and 16 B aligned (8 B records: a padded odd tail)
+          const uint32_t bytes = (RT::kPadEven ? (len + 1u) & ~1u : len) * RT::kBytes;
           mbar_expect_tx(full + s, bytes);
-          bulk_g2s(ring + (size_t)s * kPChunk, bins + (uint64_t)r * pl.capf + k0, bytes, full + s);
+          bulk_g2s(ring + (size_t)s * kCh, bins + (uint64_t)r * pl.capf + k0, bytes, full + s);
         }
       }
     }
   } else {
     // ---- consumers ----
-    const uint64_t fpmask = (1ull << pl.pb) - 1u;
     const uint32_t tab_a = saddr(tab);
     const uint64_t pol = evict_first_policy();
     // next region of this CTA with records (insert phase 1: every region, so
@@ -821,7 +905,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
     // misses go to this CTA's dense segment (warp reservation on a
     // shared-memory counter), re-binned by alternate bucket for phase 2;
     // phase-2 inserts still unplaced go to the eviction queue.  Whole warp.
-    auto settle = [&](uint32_t nm, const auto& rcs, const auto& i2s) {
+    auto settle = [&](uint32_t nm, const auto& rcs, const auto& i2s) {  // rcs: T[KK]
       constexpr int KK = sizeof(rcs) / sizeof(rcs[0]);
       (void)KK;
       if constexpr (PHASE == 1) {
@@ -842,36 +926,36 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int q = 0; q < KK; ++q)
             if ((nm >> q) & 1u)
-              *dst++ = make_uint4(ridx(rcs[q], pl.ish), (uint32_t)(rcs[q] & fpmask), (uint32_t)i2s[q],
+              *dst++ = make_uint4(RT::idx(rcs[q], pl), (uint32_t)RT::fp(rcs[q], pl), (uint32_t)i2s[q],
                                   (uint32_t)(i2s[q] >> 32));
         }
       } else if constexpr (OP == OP_INSERT && PHASE == 2) {
-        enqueue_evict_batch<KK>(sk, nm, rcs, pl.ish);
+        enqueue_evict_batch<F, KK>(sk, nm, rcs, pl);
       }
     };
     // Mutations whose single CAS attempt lost wait in this warp's retry ring
     // and are resolved 32 at a time with the full loop (a lost CAS no longer
     // re-runs the CAS body for the whole warp).  Warp-uniform head / count.
-    uint64_t* wring = retry + warp * kPRetry;
+    T* wring = retry + warp * kPRetry;
     uint32_t rhead = 0, rcount = 0;
     auto drain = [&](uint32_t mcnt, uint64_t b0r) {  // whole warp, mcnt <= 32
-      uint64_t rr[1];
+      T rr[1];
       uint64_t i2r[1] = {0};
       uint32_t nm1 = 0;
-      rr[0] = lane < mcnt ? wring[(rhead + lane) & (kPRetry - 1)] : kFiller;
+      rr[0] = lane < mcnt ? wring[(rhead + lane) & (kPRetry - 1)] : RT::filler();
       __syncwarp();
       rhead += mcnt;
       rcount -= mcnt;
       if (lane < mcnt) {
-        const uint32_t loc = (uint32_t)(rr[0] >> pl.pb) & (rb - 1u);
-        const uint64_t fp = rr[0] & fpmask;
+        const uint32_t loc = RT::off(rr[0], pl, rb - 1u);
+        const uint64_t fp = RT::fp(rr[0], pl);
         const uint32_t a = tab_a + loc * bbytes;
         const uint64_t tag = PHASE == 1 ? fp : (POL == CKF_POLICY_OFFSET ? make_tag(fp, 1u, g) : fp);
         uint64_t wv1[WPB];
         lds_bucket<WPB>(a, wv1);
         const bool done = OP == OP_INSERT ? smem_insert<F, WPB>(a, tag, wv1) : smem_remove<F, WPB>(a, tag, wv1);
         n_ok += done;
-        if (OP == OP_DELETE && PHASE == 2 && !done) clear_bit(sk.bits, ridx(rr[0], pl.ish));
+        if (OP == OP_DELETE && PHASE == 2 && !done) clear_bit(sk.bits, RT::idx(rr[0], pl));
         if (!done) {
           nm1 = 1u;
           if constexpr (PHASE == 1) {
@@ -890,24 +974,24 @@ __global__ void __launch_bounds__(kPThreads, 1)
       const uint64_t b0 = (uint64_t)r << pl.lrb;
       mbar_wait(tbar, tpar);
       tpar ^= 1u;
-      for (uint32_t k0 = 0; k0 < cn; k0 += kPChunk, ++cseq) {
+      for (uint32_t k0 = 0; k0 < cn; k0 += kCh, ++cseq) {
         const uint32_t s = cseq % kPStages;
         mbar_wait(full + s, (cseq / kPStages) & 1u);
-        const uint32_t len = min((uint32_t)kPChunk, cn - k0);
-        const uint64_t* rs = ring + (size_t)s * kPChunk + warp * (kPPerLane * 32) + lane;
-        const uint32_t kbase = warp * (kPPerLane * 32) + lane;
+        const uint32_t len = min((uint32_t)kCh, cn - k0);
+        const T* rs = ring + (size_t)s * kCh + warp * (kPL * 32) + lane;
+        const uint32_t kbase = warp * (kPL * 32) + lane;
 #pragma unroll 1
-        for (int q0 = 0; q0 < kPPerLane; q0 += kPSub<WPB>) {
-          constexpr int K = kPSub<WPB>;
-          uint64_t rc[K];
+        for (int q0 = 0; q0 < kPL; q0 += kPSub<F, WPB>) {
+          constexpr int K = kPSub<F, WPB>;
+          T rc[K];
           uint64_t wv[K][WPB];
           uint32_t vm = 0;  // bit q: record q valid
 #pragma unroll
           for (int q = 0; q < K; ++q) {
-            rc[q] = kbase + (q0 + q) * 32 < len ? rs[(q0 + q) * 32] : kFiller;
-            const bool v = !is_filler(rc[q]);  // past the chunk, or run padding
+            rc[q] = kbase + (q0 + q) * 32 < len ? rs[(q0 + q) * 32] : RT::filler();
+            const bool v = !RT::is_filler(rc[q]);  // past the chunk, or run padding
             vm |= (uint32_t)v << q;
-            const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
+            const uint32_t loc = RT::off(rc[q], pl, rb - 1u);
             // queries snapshot all buckets up front; mutations snapshot right
             // before their CAS (a stale snapshot costs a whole-warp retry)
             if (OP == OP_QUERY && v) lds_bucket_spread<WPB>(tab_a + loc * bbytes, wv[q]);
@@ -918,15 +1002,15 @@ __global__ void __launch_bounds__(kPThreads, 1)
 #pragma unroll
           for (int q = 0; q < K; ++q) {
             if (!((vm >> q) & 1u)) continue;
-            const uint32_t loc = (uint32_t)(rc[q] >> pl.pb) & (rb - 1u);
-            const uint64_t fp = rc[q] & fpmask;
-            const uint32_t idx = ridx(rc[q], pl.ish);
+            const uint32_t loc = RT::off(rc[q], pl, rb - 1u);
+            const uint64_t fp = RT::fp(rc[q], pl);
+            const uint32_t idx = RT::idx(rc[q], pl);
             if constexpr (OP == OP_QUERY) {
               const bool hit = match_any<F, WPB, POL>(wv[q], fp);
               if (hit && !dflt) set_bit(sk.bits, idx);
               if (PHASE == 2 && !hit && dflt) clear_bit(sk.bits, idx);  // a final negative
               if (PHASE == 1 && !hit && !dflt) {  // dual records: the i2 record is binned already
-                n_alt += !ralt(rc[q], pl.ish);
+                n_alt += !RT::alt(rc[q], pl);
               } else if (PHASE == 1 && !hit) {
                 nm |= 1u << q;
                 uint64_t cc;

@@ -106,8 +106,9 @@ def test_workspace_sizing():
     assert L.ckf_workspace_bytes(ctypes.byref(big), n, _lib.OP_QUERY, _lib.FORCE_DIRECT) == 0
     b4 = FilterConfig(bucket_count=1 << 24, bucket_slots=4).ckf_params()  # 8-byte buckets: regions of 2^14
     assert L.ckf_workspace_bytes(ctypes.byref(b4), n, _lib.OP_QUERY, _lib.FORCE_TILED) > 0
-    f32 = FilterConfig(bucket_count=1 << 24, fingerprint_bits=32).ckf_params()  # a record has no room for f=32
-    assert L.ckf_workspace_bytes(ctypes.byref(f32), n, _lib.OP_QUERY, _lib.FORCE_TILED) == 0
+    f32 = FilterConfig(bucket_count=1 << 24, fingerprint_bits=32).ckf_params()  # 16-byte records
+    w32 = L.ckf_workspace_bytes(ctypes.byref(f32), n, _lib.OP_QUERY, _lib.FORCE_TILED)
+    assert w32 > 1.5 * wq  # twice the record bytes
 
 
 @pytest.mark.parametrize("lm", [24, 25, 26, 27])
