@@ -168,3 +168,28 @@ def test_offset_alt_round_trip_host():
                 assert c == 1 and 0 <= j < m and j != i
                 back, c2 = alt_index(j, fp, 1, cfg)
                 assert (back, c2) == (i, 0)
+
+
+def test_automatic_schedule_follows_measured_crossovers():
+    """Region from 1 key per bucket for insert / delete and 2 for lookups with
+    32-byte buckets, 1.5 for every op with 64-byte buckets (f = 32); small
+    (L2-resident) tables always direct (profiles/r02_crossover.jsonl)."""
+    L = _lib.lib()
+
+    def sched(cfg, n, op):
+        p = cfg.ckf_params()
+        w = L.ckf_workspace_bytes(ctypes.byref(p), n, op, 0)
+        runs = ctypes.c_uint64(0)
+        return L.ckf_schedule(ctypes.byref(p), n, op, 0, 8, 256, w, ctypes.byref(runs))
+
+    f16 = FilterConfig(bucket_count=1 << 24)
+    m = f16.bucket_count
+    R, D = _lib.SCHED_REGION, _lib.SCHED_DIRECT
+    assert sched(f16, m - 1, _lib.OP_INSERT) == D and sched(f16, m, _lib.OP_INSERT) == R
+    assert sched(f16, m, _lib.OP_DELETE) == R
+    assert sched(f16, 2 * m - 1, _lib.OP_QUERY) == D and sched(f16, 2 * m, _lib.OP_QUERY) == R
+    f32 = FilterConfig(bucket_count=1 << 24, fingerprint_bits=32)
+    for op in (_lib.OP_INSERT, _lib.OP_QUERY, _lib.OP_DELETE):
+        assert sched(f32, m, op) == D and sched(f32, 3 * m // 2, op) == R
+    small = FilterConfig(bucket_count=1 << 18)
+    assert sched(small, 100 * small.bucket_count, _lib.OP_INSERT) == D
