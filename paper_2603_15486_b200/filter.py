@@ -547,6 +547,15 @@ class CuckooFilter:
     # chunk i+1 is copied in while chunk i is processed and chunk i-1's answers
     # are copied out (PCIe is the bound for host data: ~55 GB/s each way).
     HOST_CHUNK = 1 << 25
+    # The last chunk is cut short: once its keys are in, the H2D link idles
+    # until the call returns (its kernels + its answers' D2H), so a small
+    # tail keeps that bubble to ~0.2 ms instead of a whole chunk's compute.
+    HOST_TAIL = 1 << 22
+
+    def _chunk_bounds(self, n: int) -> list:
+        body = max(n - self.HOST_TAIL, 0)
+        cuts = list(range(0, body, self.HOST_CHUNK)) + [body, n]
+        return [(lo, hi) for lo, hi in zip(cuts, cuts[1:]) if hi > lo]
 
     def _host_pipeline(self, op: int, keys: torch.Tensor, flags: int, p=None):
         """Chunked H2D -> kernel -> D2H with copy/compute overlap for CPU keys.
@@ -565,8 +574,8 @@ class CuckooFilter:
         ans = torch.empty(n, dtype=torch.bool, pin_memory=True)
         parts = []
         free_in, free_out = [None, None], [None, None]
-        for ci, lo in enumerate(range(0, n, C)):
-            hi, b = min(n, lo + C), ci & 1
+        for ci, (lo, hi) in enumerate(self._chunk_bounds(n)):
+            b = ci & 1
             m = hi - lo
             with torch.cuda.stream(P["in"]):
                 if free_in[b] is not None:

@@ -123,3 +123,16 @@ def _blob(magic=b"CKGF", version=1, f=16, b=16, m=64, pol=0, occ=0, seed=0, word
 def test_from_bytes_rejects_corruption(blob, match):
     with pytest.raises(ValueError, match=match):
         CuckooFilter.from_bytes(blob)
+
+
+@pytest.mark.parametrize("n", [1, 5, 1 << 10, (1 << 10) + 1, 1 << 12, (1 << 12) + 3, 10_000, 1 << 16])
+def test_host_chunk_bounds_cover_batch_with_short_tail(monkeypatch, n):
+    """Host pipeline chunking: contiguous, covers [0, n), no chunk above
+    HOST_CHUNK, and the last chunk is at most HOST_TAIL keys."""
+    monkeypatch.setattr(CuckooFilter, "HOST_CHUNK", 1 << 12)
+    monkeypatch.setattr(CuckooFilter, "HOST_TAIL", 1 << 10)
+    b = CuckooFilter._chunk_bounds(CuckooFilter.__new__(CuckooFilter), n)
+    assert b[0][0] == 0 and b[-1][1] == n
+    assert all(hi > lo for lo, hi in b) and all(x[1] == y[0] for x, y in zip(b, b[1:]))
+    assert max(hi - lo for lo, hi in b) <= 1 << 12
+    assert b[-1][1] - b[-1][0] <= 1 << 10
