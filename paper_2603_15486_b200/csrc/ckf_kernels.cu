@@ -237,6 +237,31 @@ __global__ void __launch_bounds__(kBlock, kEvictBlocks) evict_kernel(Geo g, uint
   block_count_add(n_ok, 0, ctr, occ, +1);
 }
 
+// Room map of the whole table for the direct insert path (a bit per bucket:
+// has an empty lane), built after insert_kernel so the BFS eviction pass can
+// read its candidates' room from L2 the way the region schedule's does.
+// Used for L2-resident tables only (the scan is one pass over the table).
+template <int F, int WPB>
+__global__ void __launch_bounds__(kBlock) room_scan_kernel(const uint64_t* __restrict__ words, uint64_t m,
+                                                           uint32_t* __restrict__ bits,
+                                                           unsigned long long* __restrict__ cursor) {
+  if (blockIdx.x == 0 && threadIdx.x == 0) *cursor = 0;  // the eviction pass's queue cursor
+  const uint64_t nw = (m + 31) / 32;
+  for (uint64_t b0 = (blockIdx.x * (uint64_t)kBlock + threadIdx.x) & ~31ull; b0 < nw * 32;
+       b0 += (uint64_t)gridDim.x * kBlock) {
+    const uint64_t b = b0 + (threadIdx.x & 31);
+    bool room = false;
+    if (b < m) {
+      uint64_t any = 0;
+#pragma unroll
+      for (int j = 0; j < WPB; ++j) any |= Lanes<F>::zeros(__ldcg(words + b * WPB + j));
+      room = any != 0;
+    }
+    const unsigned bal = __ballot_sync(0xffffffffu, room);
+    if ((threadIdx.x & 31) == 0) bits[b0 >> 5] = bal;
+  }
+}
+
 // BFS eviction pass of the region schedule, one ROUND at a time per lane.
 // The chains of a warp's 32 queued keys differ in length (at 95 % load: mean
 // 1.11 rounds, mean warp maximum 2.23; profiles/r02_evict_rounds.txt), so
@@ -642,6 +667,7 @@ constexpr uint64_t kRegionMinTable = 48ull << 20;  // below this the table is L2
 constexpr uint32_t kMaxF2 = 512;                   // fine regions per coarse region (split bins)
 
 static uint64_t align256(uint64_t x) { return (x + 255) & ~255ull; }
+static uint64_t direct_rm_bytes(uint64_t m) { return align256((m + 31) / 32 * 4); }
 
 // Developer knobs: CKF_REGION_KB (fine-region bytes), CKF_TILED_AUTO (0
 // disables the automatic choice of the region schedule), CKF_MAX_RUN_KEYS (a
@@ -860,6 +886,7 @@ struct TiledArgs {
   RPlan rpl;
   RLayout RL;
   void* ws;
+  bool direct_rm;  // direct insert: ws holds a room map + eviction cursor (direct_ws_bytes)
 };
 
 // the call's keys in runs of at most pl.chunk: (offset, count) of run k
@@ -980,7 +1007,23 @@ struct InsertOp {
                                                          a.cap, a.ctr, a.occ, a.hashed);
     int st = status();
     if (st) return st;
-    return a.cap ? launch_evict<F, WPB, POL>(a, 0, nullptr, RoomMap{nullptr}) : CKF_OK;
+    if (!a.cap) return CKF_OK;
+    if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
+      if (a.t.direct_rm && a.g.eviction == CKF_EVICT_BFS) {
+        // room map of the filled table + BFS eviction one round per lane
+        // (evict_bfs_kernel), as on the region schedule
+        // (two launches: the scan also zeroes the cursor)
+        uint32_t* bits = (uint32_t*)a.t.ws;
+        unsigned long long* cur = (unsigned long long*)((char*)a.t.ws + direct_rm_bytes(a.g.m));
+        const uint64_t nw = (a.g.m + 31) / 32;
+        room_scan_kernel<F, WPB><<<grid_for(nw * 32, kBlock, 16), kBlock, 0, a.s>>>(a.words, a.g.m, bits, cur);
+        if ((st = status())) return st;
+        evict_bfs_kernel<F, WPB, POL><<<(unsigned)sm_count() * kEvictBlocks, kBlock, 0, a.s>>>(
+            a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ, a.keys, a.hashed, 0, cur, RoomMap{bits});
+        return status();
+      }
+    }
+    return launch_evict<F, WPB, POL>(a, 0, nullptr, RoomMap{nullptr});
   }
 };
 
@@ -1471,11 +1514,35 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
   return t;
 }
 
-uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
-  if (!params_ok(p) || !region_wanted(p, n, op, flags)) return 0;
+// Direct-path insert scratch: a room map (one bit per bucket) and the BFS
+// eviction cursor, for batches of >= m/8 keys into L2-resident tables (the
+// map costs one scan of the table).  Measured (profiles/r02_direct_roommap.txt):
+// 2^22 slots f=16 b=16 insert 0.277 -> 0.250 ms, 2^24 slots 0.779 -> 0.705 ms;
+// one-word buckets (b=4: the pass is bound by its longest chain) 2 % slower,
+// so they keep the one-chain-per-thread pass.
+static uint64_t direct_ws_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
+  if (op != CKF_OP_INSERT || (flags & CKF_MODE_SEQUENTIAL) || p->eviction != CKF_EVICT_BFS) return 0;
+  const uint32_t wpb = p->words_per_bucket;
+  if (wpb != 2 && wpb != 4 && wpb != 8) return 0;
+  const uint64_t m = p->bucket_count;
+  if (m * wpb * 8ull > kRegionMinTable || n * 8 < m || env_u64("CKF_NO_DIRECT_ROOM_MAP", 0)) return 0;
+  return direct_rm_bytes(m) + 256;
+}
+
+static bool region_planned(const ckf_params* p, uint64_t n, int op, unsigned flags) {
+  if (!region_wanted(p, n, op, flags)) return false;
   bool ok;
-  const RPlan rp = make_rplan(p, n, op, flags, ok);
-  return ok ? rlayout_for(rp, op).total : 0;
+  make_rplan(p, n, op, flags, ok);
+  return ok;
+}
+
+uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags) {
+  if (!params_ok(p)) return 0;
+  if (region_planned(p, n, op, flags)) {
+    bool ok;
+    return rlayout_for(make_rplan(p, n, op, flags, ok), op).total;
+  }
+  return direct_ws_bytes(p, n, op, flags);
 }
 
 int ckf_schedule(const ckf_params* p, uint64_t n, int op, unsigned flags, const void* keys, const void* workspace,
@@ -1483,7 +1550,7 @@ int ckf_schedule(const ckf_params* p, uint64_t n, int op, unsigned flags, const 
   if (runs) *runs = 0;
   if (!params_ok(p)) return CKF_EINVAL;
   if (flags & CKF_MODE_SEQUENTIAL) return op == CKF_OP_QUERY ? CKF_SCHED_DIRECT : CKF_SCHED_SEQUENTIAL;
-  if (ckf_workspace_bytes(p, n, op, flags) == 0) return CKF_SCHED_DIRECT;
+  if (!region_planned(p, n, op, flags)) return CKF_SCHED_DIRECT;
   const TiledArgs t = choose(p, n, op, flags, keys, const_cast<void*>(workspace), workspace_bytes);
   if (!t.region) return CKF_SCHED_DIRECT;
   if (runs) *runs = run_count(t, n);
@@ -1501,6 +1568,13 @@ int ckf_insert(const ckf_params* p, uint64_t* words, const uint64_t* keys, uint6
   InsertArgs a{geo_from(*p), words, keys, n, ok, evictions, lost, records, records ? record_cap : 0,
                counters, occupancy, (flags & CKF_INPUT_HASHED) != 0, (flags & CKF_MODE_SEQUENTIAL) != 0, s,
                choose(p, n, CKF_OP_INSERT, flags, keys, workspace, workspace_bytes)};
+  if (!a.t.region && workspace && ((uintptr_t)workspace % 256) == 0) {
+    const uint64_t need = direct_ws_bytes(p, n, CKF_OP_INSERT, flags);
+    if (need && workspace_bytes >= need) {
+      a.t.ws = workspace;
+      a.t.direct_rm = true;
+    }
+  }
   return dispatch3<InsertOp>(p, words, a);
 }
 

@@ -193,3 +193,26 @@ def test_automatic_schedule_follows_measured_crossovers():
         assert sched(f32, m, op) == D and sched(f32, 3 * m // 2, op) == R
     small = FilterConfig(bucket_count=1 << 18)
     assert sched(small, 100 * small.bucket_count, _lib.OP_INSERT) == D
+
+
+def test_direct_insert_room_map_workspace():
+    """Direct-path inserts into L2-resident tables ask for a room map (a bit
+    per bucket) + the eviction cursor, and still run the direct schedule;
+    one-word buckets, DFS, parity mode and small batches ask for nothing."""
+    L = _lib.lib()
+    runs = ctypes.c_uint64(0)
+
+    def ws(cfg, n, op=_lib.OP_INSERT, flags=0):
+        return L.ckf_workspace_bytes(ctypes.byref(cfg.ckf_params()), n, op, flags)
+
+    cfg = FilterConfig(bucket_count=1 << 18, eviction="bfs")
+    m, n = cfg.bucket_count, int(0.95 * cfg.total_slots)
+    w = ws(cfg, n)
+    assert m // 8 <= w <= m // 8 + 512
+    p = cfg.ckf_params()
+    assert L.ckf_schedule(ctypes.byref(p), n, _lib.OP_INSERT, 0, 8, 256, w, ctypes.byref(runs)) == _lib.SCHED_DIRECT
+    assert ws(cfg, n, _lib.OP_QUERY) == 0 and ws(cfg, n, _lib.OP_DELETE) == 0
+    assert ws(cfg, m // 8 - 1) == 0 and ws(cfg, n, flags=_lib.MODE_SEQUENTIAL) == 0
+    assert ws(FilterConfig(bucket_count=1 << 18, eviction="dfs"), n) == 0
+    assert ws(FilterConfig(bucket_count=1 << 18, bucket_slots=4), n) == 0  # chain-tail bound: no map
+    assert ws(FilterConfig(bucket_count=1 << 21, eviction="bfs"), 1 << 19) == 0  # 64 MiB table: not L2-resident
