@@ -851,19 +851,33 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   constexpr uint32_t kBinSmem = sizeof(BinSmem<F>);
   constexpr uint32_t kProbeSmemF = kProbeSmem<F>;
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS>>(kBinSmem);
+  if constexpr (OP == OP_QUERY) allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_KEYS_DUAL>>(kBinSmem);
   allow_big_smem<region_bin_kernel<OP, F, WPB, POL, SRC_MISS>>(kBinSmem);
   allow_big_smem<region_split_kernel<OP, F, WPB, POL>>(kBinSmem);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1>>(kProbeSmemF);
   allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2>>(kProbeSmemF);
+  if constexpr (OP == OP_QUERY) {
+    allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 1, 0>>(kProbeSmemF);
+    allow_big_smem<region_probe_kernel<OP, F, WPB, POL, 2, 0>>(kProbeSmemF);
+  }
   int st;
   // phase 1: primary buckets
   region_bin_kernel<OP, F, WPB, POL, SRC_KEYS><<<grid_for(n, kBTile, kBinBlocks), kBThreads, kBinSmem, s>>>(
       g, pl, words, keys, n, hashed, w, sk, mocc);
   if ((st = status())) return st;
+  if constexpr (OP == OP_QUERY) {  // (exits unless the sample chose dual records)
+    region_bin_kernel<OP, F, WPB, POL, SRC_KEYS_DUAL><<<grid_for(n, kBTile, kBinBlocks), kBThreads, kBinSmem, s>>>(
+        g, pl, words, keys, n, hashed, w, sk, mocc);
+    if ((st = status())) return st;
+  }
   region_split_kernel<OP, F, WPB, POL><<<sms * kSplitBlocks, kBThreads, kBinSmem, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 1><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
+  if constexpr (OP == OP_QUERY) {  // (exits unless the results start all-false)
+    region_probe_kernel<OP, F, WPB, POL, 1, 0><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
+    if ((st = status())) return st;
+  }
   // phase 2: the misses, on their alternate buckets
   if (cudaMemsetAsync(ws, 0, L.bin_ctr_end, s) != cudaSuccess) return cuda_error();
   region_bin_kernel<OP, F, WPB, POL, SRC_MISS><<<dim3((sms * kBinBlocks + pg - 1) / pg, pg), kBThreads, kBinSmem, s>>>(
@@ -873,6 +887,10 @@ static int run_region(const Geo& g, const RPlan& pl, const RLayout& L, void* ws,
   if ((st = status())) return st;
   region_probe_kernel<OP, F, WPB, POL, 2><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
   if ((st = status())) return st;
+  if constexpr (OP == OP_QUERY) {
+    region_probe_kernel<OP, F, WPB, POL, 2, 0><<<pg, kPThreads, kProbeSmemF, s>>>(g, pl, words, w, sk, mocc);
+    if ((st = status())) return st;
+  }
   if (OP != OP_INSERT) {
     expand_count_kernel<<<grid_for((n + 31) / 32, 256, 8), 256, 0, s>>>(w.bits, n, out,
                                                                        OP == OP_QUERY ? sk.ctr : nullptr);

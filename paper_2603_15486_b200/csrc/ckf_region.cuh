@@ -510,7 +510,7 @@ __device__ __forceinline__ void bin_release() { bulk_wait_read(); }
 // SRC_KEYS: the batch's keys (or hashes), one record per key for its primary
 // bucket.  SRC_MISS: phase-1 misses {idx, fp, i2} from probe-CTA segment
 // blockIdx.y, one record for the alternate bucket.
-enum { SRC_KEYS = 0, SRC_MISS = 1 };
+enum { SRC_KEYS = 0, SRC_MISS = 1, SRC_KEYS_DUAL = 2 };
 
 #ifndef CKF_BIN_BLOCKS
 #define CKF_BIN_BLOCKS 3  // (measured: 4 per SM -- 64 registers, spills -- is slower)
@@ -527,18 +527,23 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
   BinSmem<F>& sm = *reinterpret_cast<BinSmem<F>*>(bsm_raw);
   // dual: a query batch sampled as mostly negative gets an i1 AND an i2 record
   // per key here (no phase 2); the tile then holds kBTile / 2 keys
-  const bool dual = OP == OP_QUERY && SRC == SRC_KEYS && w.mode[0] == 0;
+  constexpr bool kKeys = SRC != SRC_MISS;
+  constexpr bool dual = OP == OP_QUERY && SRC == SRC_KEYS_DUAL;
+  // query batches launch both key variants; the one that does not match the
+  // sampled mode exits (dual is a compile-time property of the tile loop)
+  if constexpr (OP == OP_QUERY && kKeys)
+    if ((w.mode[0] == 0) != dual) return;
   const uint64_t KT = dual ? kBTile / 2 : kBTile;  // keys (items) per tile
   const uint64_t pol = evict_first_policy();
   const uint32_t lmask = (1u << pl.lrbc) - 1u;
-  const uint64_t n = SRC == SRC_KEYS ? n_keys : w.n_miss[blockIdx.y];
+  const uint64_t n = kKeys ? n_keys : w.n_miss[blockIdx.y];
   const bool al16 = ((uintptr_t)keys & 15) == 0;  // 256-bit pair loads need 16 B alignment
   const uint4* ms = w.miss + (uint64_t)blockIdx.y * w.seg;
   uint32_t n_ok = 0, n_alt = 0;
   for (uint64_t t0 = blockIdx.x * KT; t0 < n; t0 += (uint64_t)gridDim.x * KT) {
     if (threadIdx.x == 0) {
       const uint64_t nx = t0 + (uint64_t)gridDim.x * KT;
-      if (SRC == SRC_KEYS && nx < n && n - nx >= 4) {  // 16 B-aligned window inside the next tile
+      if (kKeys && nx < n && n - nx >= 4) {  // 16 B-aligned window inside the next tile
         const uintptr_t lo = ((uintptr_t)(keys + nx) + 15) & ~(uintptr_t)15;
         const uintptr_t hi = (uintptr_t)(keys + nx + min(KT, n - nx)) & ~(uintptr_t)15;
         if (hi > lo) prefetch_l2((const void*)lo, (uint32_t)(hi - lo));
@@ -548,7 +553,7 @@ __global__ void __launch_bounds__(kBThreads, kBinBlocks)
     for (uint32_t r = threadIdx.x; r < pl.R1; r += kBThreads) sm.cnt[r] = 0;
     T rec[kBItems];
     uint32_t pk[kBItems];  // bin << 16 | rank; 0xFFFFFFFF = no record
-    if constexpr (SRC == SRC_KEYS) {
+    if constexpr (kKeys) {
       // item q of thread t: key t0 + (q / 2) * 2 * kBThreads + 2t + (q % 2) (pairs
       // of 16 B, coalesced); dual: items [0, kBItems/2) are keys, the rest
       // their i2 records.  The record's index field advances by a running
@@ -818,9 +823,15 @@ __device__ __forceinline__ void enqueue_evict_batch(const Sink& sk, uint32_t nm,
 // mbarriers.  Warps 0..kPWarps-1 consume: each owns a fixed slice of every
 // chunk, so they never wait for each other except at region boundaries, where
 // consumer thread 0 writes the table slice back and loads the next one.
-template <int OP, int F, int WPB, int POL, int PHASE>
+// DF: the results' starting value (RWork::mode) as a compile-time constant --
+// mutations always 1; query batches launch both variants and the one that does
+// not match the sampled mode exits.
+template <int OP, int F, int WPB, int POL, int PHASE, int DF = 1>
 __global__ void __launch_bounds__(kPThreads, 1)
     region_probe_kernel(Geo g, RPlan pl, uint64_t* words, RWork w, Sink sk, long long* occ) {
+  static_assert(OP == OP_QUERY || DF == 1, "mutations start from all-true results");
+  if constexpr (OP == OP_QUERY)
+    if ((*w.mode != 0) != (DF != 0)) return;
   using RT = RecT<F>;
   using T = typename RT::T;
   constexpr int kPL = kPPerLane<F>, kCh = kPChunk<F>;
@@ -838,7 +849,7 @@ __global__ void __launch_bounds__(kPThreads, 1)
   const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
   const uint32_t rb = 1u << pl.lrb;
   constexpr uint32_t bbytes = WPB * 8;
-  const bool dflt = OP == OP_QUERY ? *w.mode != 0 : true;  // results' starting value (see RWork::mode)
+  constexpr bool dflt = DF != 0;  // results' starting value (see RWork::mode)
   if (tid == 0) {
     for (int s = 0; s < kPStages; ++s) {
       mbar_init(full + s, 1);
