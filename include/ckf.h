@@ -136,10 +136,12 @@ int ckf_hash(const uint64_t* keys, uint64_t n, uint64_t seed, uint64_t* out, voi
 int ckf_place(const ckf_params* p, const uint64_t* keys, uint64_t n, uint64_t* fp, uint64_t* i1,
               uint64_t* i2, unsigned flags, void* stream);
 
-/* Scratch bytes for which a batch of n keys runs the region schedule (keys
- * binned by table region, every bucket access in shared memory).
- * 0 means this batch runs on the direct kernels and needs no workspace.
- * Passing a smaller (or NULL) workspace to an op also selects the direct path. */
+/* Scratch bytes a batch of n keys wants: the region schedule's (keys binned
+ * by table region, every bucket access in shared memory), or,
+ * for a direct-path BFS insert into an L2-resident table, a room map (one bit
+ * per bucket) + the eviction cursor.  0: direct kernels, no workspace.
+ * Passing a smaller (or NULL) workspace selects the direct path without the
+ * room map; ckf_schedule reports which schedule runs. */
 uint64_t ckf_workspace_bytes(const ckf_params* p, uint64_t n, int op, unsigned flags);
 
 /* The schedule (CKF_SCHED_*) an op call with these arguments runs, and in how
