@@ -209,12 +209,11 @@ constexpr int kEvictBlocks = CKF_EVICT_BLOCKS;  // resident blocks per SM (<= 85
 // Queue entries [*qstart, n_queued) belong to this run (a chunk of the call
 // whose keys start at batch index ibase; keys / ok / ev / lost are the run's).
 template <int F, int WPB, int POL>
-__global__ void __launch_bounds__(kBlock, kEvictBlocks) evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
-                                                       int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
-                                                       ckf_record* __restrict__ rec, uint64_t cap,
-                                                       ckf_counters* ctr, long long* occ,
-                                                       const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
-                                                       const unsigned long long* qstart, RoomMap rm) {
+__device__ __forceinline__ void evict_chains_body(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
+                                                  int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
+                                                  ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                                                  long long* occ, const uint64_t* __restrict__ keys, bool hashed,
+                                                  uint64_t ibase, const unsigned long long* qstart, RoomMap rm) {
   const unsigned long long queued = *(volatile unsigned long long*)&ctr->n_queued;
   const uint64_t cnt = queued < cap ? queued : cap;
   const uint64_t r0 = qstart ? *qstart : 0;
@@ -237,15 +236,37 @@ __global__ void __launch_bounds__(kBlock, kEvictBlocks) evict_kernel(Geo g, uint
   block_count_add(n_ok, 0, ctr, occ, +1);
 }
 
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBlock, kEvictBlocks)
+    evict_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok, int64_t* __restrict__ ev,
+                 uint64_t* __restrict__ lost, ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                 long long* occ, const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
+                 const unsigned long long* qstart, RoomMap rm) {
+  evict_chains_body<F, WPB, POL>(g, words, ok, ev, lost, rec, cap, ctr, occ, keys, hashed, ibase, qstart, rm);
+}
+
 // Room map of the whole table for the direct insert path (a bit per bucket:
 // has an empty lane), built after insert_kernel so the BFS eviction pass can
 // read its candidates' room from L2 the way the region schedule's does.
 // Used for L2-resident tables only (the scan is one pass over the table).
+// The map pays off once the eviction queue is long enough: built (gate = 1)
+// when n_queued * kRoomMapBytesPerKey >= the table's bytes, else the chain pass
+// runs (profiles/r02_direct_roommap.txt: a 4 Mi-key insert into a 2^28-slot
+// table at 95 % load, 1.9 M queued: 0.90 -> 0.70 ms with the map).
+constexpr uint64_t kRoomMapBytesPerKey = 512;
 template <int F, int WPB>
 __global__ void __launch_bounds__(kBlock) room_scan_kernel(const uint64_t* __restrict__ words, uint64_t m,
                                                            uint32_t* __restrict__ bits,
-                                                           unsigned long long* __restrict__ cursor) {
-  if (blockIdx.x == 0 && threadIdx.x == 0) *cursor = 0;  // the eviction pass's queue cursor
+                                                           unsigned long long* __restrict__ cursor,
+                                                           const ckf_counters* ctr,
+                                                           unsigned long long* __restrict__ gate) {
+  const unsigned long long queued = *(volatile const unsigned long long*)&ctr->n_queued;
+  const bool use = queued * kRoomMapBytesPerKey >= m * WPB * 8ull;
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    *cursor = 0;  // the eviction pass's queue cursor
+    *gate = use;
+  }
+  if (!use) return;
   const uint64_t nw = (m + 31) / 32;
   for (uint64_t b0 = (blockIdx.x * (uint64_t)kBlock + threadIdx.x) & ~31ull; b0 < nw * 32;
        b0 += (uint64_t)gridDim.x * kBlock) {
@@ -271,11 +292,11 @@ __global__ void __launch_bounds__(kBlock) room_scan_kernel(const uint64_t* __res
 // queue entry (warp-aggregated cursor), so the warp stays full.  Candidates'
 // room comes from the room map (RoomMap, ckf_device.cuh).
 template <int F, int WPB, int POL>
-__global__ void __launch_bounds__(kBlock, kEvictBlocks)
-    evict_bfs_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok, int64_t* __restrict__ ev,
-                     uint64_t* __restrict__ lost, ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
-                     long long* occ, const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
-                     unsigned long long* cursor, RoomMap rm) {
+__device__ __forceinline__ void evict_bfs_body(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok,
+                                               int64_t* __restrict__ ev, uint64_t* __restrict__ lost,
+                                               ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                                               long long* occ, const uint64_t* __restrict__ keys, bool hashed,
+                                               uint64_t ibase, unsigned long long* cursor, RoomMap rm) {
   using L = Lanes<F>;
   constexpr int kTpw = L::kTpw;
   constexpr uint32_t kB = WPB * kTpw;
@@ -409,6 +430,31 @@ __global__ void __launch_bounds__(kBlock, kEvictBlocks)
   }
   if (threadIdx.x == 0 && blockIdx.x == 0) ctr->n_records = total;
   block_count_add(n_ok, 0, ctr, occ, +1);
+}
+
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBlock, kEvictBlocks)
+    evict_bfs_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok, int64_t* __restrict__ ev,
+                     uint64_t* __restrict__ lost, ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                     long long* occ, const uint64_t* __restrict__ keys, bool hashed, uint64_t ibase,
+                     unsigned long long* cursor, RoomMap rm) {
+  evict_bfs_body<F, WPB, POL>(g, words, ok, ev, lost, rec, cap, ctr, occ, keys, hashed, ibase, cursor, rm);
+}
+
+// Direct-path eviction in one launch: room_scan_kernel decided on the device
+// whether the room map was worth building (gate) -- BFS rounds with the map
+// and queue refill, or one chain per thread.
+template <int F, int WPB, int POL>
+__global__ void __launch_bounds__(kBlock, kEvictBlocks)
+    evict_direct_kernel(Geo g, uint64_t* __restrict__ words, uint8_t* __restrict__ ok, int64_t* __restrict__ ev,
+                        uint64_t* __restrict__ lost, ckf_record* __restrict__ rec, uint64_t cap, ckf_counters* ctr,
+                        long long* occ, const uint64_t* __restrict__ keys, bool hashed, unsigned long long* cursor,
+                        RoomMap rm, const unsigned long long* gate) {
+  if (*gate)
+    evict_bfs_body<F, WPB, POL>(g, words, ok, ev, lost, rec, cap, ctr, occ, keys, hashed, 0, cursor, rm);
+  else
+    evict_chains_body<F, WPB, POL>(g, words, ok, ev, lost, rec, cap, ctr, occ, keys, hashed, 0, nullptr,
+                                   RoomMap{nullptr});
 }
 
 // Delete (K:461-484): full-lane match, i1 with fp, then i2 with fp|choice.
@@ -1028,16 +1074,20 @@ struct InsertOp {
     if (!a.cap) return CKF_OK;
     if constexpr (WPB == 2 || WPB == 4 || WPB == 8) {
       if (a.t.direct_rm && a.g.eviction == CKF_EVICT_BFS) {
-        // room map of the filled table + BFS eviction one round per lane
-        // (evict_bfs_kernel), as on the region schedule
-        // (two launches: the scan also zeroes the cursor)
+        // room map of the filled table + BFS eviction one round per lane, as
+        // on the region schedule -- when the queue is long enough (the scan
+        // decides on the device, sets the gate evict_direct_kernel branches
+        // on, and zeroes the cursor)
         uint32_t* bits = (uint32_t*)a.t.ws;
         unsigned long long* cur = (unsigned long long*)((char*)a.t.ws + direct_rm_bytes(a.g.m));
         const uint64_t nw = (a.g.m + 31) / 32;
-        room_scan_kernel<F, WPB><<<grid_for(nw * 32, kBlock, 16), kBlock, 0, a.s>>>(a.words, a.g.m, bits, cur);
+        const unsigned eg = (unsigned)sm_count() * kEvictBlocks;
+        room_scan_kernel<F, WPB><<<grid_for(nw * 32, kBlock, 16), kBlock, 0, a.s>>>(a.words, a.g.m, bits, cur,
+                                                                                    a.ctr, cur + 1);
         if ((st = status())) return st;
-        evict_bfs_kernel<F, WPB, POL><<<(unsigned)sm_count() * kEvictBlocks, kBlock, 0, a.s>>>(
-            a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap, a.ctr, a.occ, a.keys, a.hashed, 0, cur, RoomMap{bits});
+        evict_direct_kernel<F, WPB, POL><<<eg, kBlock, 0, a.s>>>(a.g, a.words, a.ok, a.ev, a.lost, a.rec, a.cap,
+                                                                 a.ctr, a.occ, a.keys, a.hashed, cur, RoomMap{bits},
+                                                                 cur + 1);
         return status();
       }
     }
@@ -1532,9 +1582,10 @@ static TiledArgs choose(const ckf_params* p, uint64_t n, int op, unsigned flags,
   return t;
 }
 
-// Direct-path insert scratch: a room map (one bit per bucket) and the BFS
-// eviction cursor, for batches of >= m/8 keys into L2-resident tables (the
-// map costs one scan of the table).  Measured (profiles/r02_direct_roommap.txt):
+// Direct-path insert scratch: a room map (one bit per bucket), the BFS
+// eviction cursor and the gate, for batches of >= m/8 keys (the map costs one
+// scan of the table; room_scan_kernel builds it only for a long enough
+// eviction queue).  Measured (profiles/r02_direct_roommap.txt):
 // 2^22 slots f=16 b=16 insert 0.277 -> 0.250 ms, 2^24 slots 0.779 -> 0.705 ms;
 // one-word buckets (b=4: the pass is bound by its longest chain) 2 % slower,
 // so they keep the one-chain-per-thread pass.
@@ -1543,7 +1594,7 @@ static uint64_t direct_ws_bytes(const ckf_params* p, uint64_t n, int op, unsigne
   const uint32_t wpb = p->words_per_bucket;
   if (wpb != 2 && wpb != 4 && wpb != 8) return 0;
   const uint64_t m = p->bucket_count;
-  if (m * wpb * 8ull > kRegionMinTable || n * 8 < m || env_u64("CKF_NO_DIRECT_ROOM_MAP", 0)) return 0;
+  if (n * 8 < m || env_u64("CKF_NO_DIRECT_ROOM_MAP", 0)) return 0;
   return direct_rm_bytes(m) + 256;
 }
 

@@ -196,9 +196,10 @@ def test_automatic_schedule_follows_measured_crossovers():
 
 
 def test_direct_insert_room_map_workspace():
-    """Direct-path inserts into L2-resident tables ask for a room map (a bit
-    per bucket) + the eviction cursor, and still run the direct schedule;
-    one-word buckets, DFS, parity mode and small batches ask for nothing."""
+    """Direct-path BFS inserts of >= m/8 keys ask for a room map (a bit per
+    bucket) + the eviction cursor and gate (the device builds the map only for
+    a long eviction queue), and still run the direct schedule; one-word
+    buckets, DFS, parity mode and small batches ask for nothing."""
     L = _lib.lib()
     runs = ctypes.c_uint64(0)
 
@@ -215,4 +216,5 @@ def test_direct_insert_room_map_workspace():
     assert ws(cfg, m // 8 - 1) == 0 and ws(cfg, n, flags=_lib.MODE_SEQUENTIAL) == 0
     assert ws(FilterConfig(bucket_count=1 << 18, eviction="dfs"), n) == 0
     assert ws(FilterConfig(bucket_count=1 << 18, bucket_slots=4), n) == 0  # chain-tail bound: no map
-    assert ws(FilterConfig(bucket_count=1 << 21, eviction="bfs"), 1 << 19) == 0  # 64 MiB table: not L2-resident
+    big = FilterConfig(bucket_count=1 << 21, eviction="bfs")  # 64 MiB: the map is gated on the queue length
+    assert (1 << 21) // 8 <= ws(big, 1 << 19) <= (1 << 21) // 8 + 512
